@@ -1,0 +1,163 @@
+/*
+ * ut.h — C ABI of the B200 unified-tensor gather (PyTorch-Direct, arXiv 2101.07956).
+ *
+ * The operation. PyTorch-Direct keeps the node-feature table in host memory as a "unified
+ * tensor" that GPU threads dereference directly over the host link (PAPER.md:239-243,
+ * §3 Fig. 2b; §4.1), and its hot path is "indexing unified tensor with GPU
+ * tensor", `unified_tensor[gpu_tensor]` (Table 1; Listing 2),
+ * whose output is a GPU tensor (Table 3 row 2 / col 1). The feature table is
+ * "a 2D array where the row indices are the IDs of nodes and the columns are the features of
+ * each node". This library computes exactly
+ *
+ *     for i in [0, n):  out[i*rb .. (i+1)*rb) = table[idx[i]*rb .. (idx[i]+1)*rb)
+ *
+ * byte for byte (rb = row_bytes), with GPU threads reading the rows straight out of the
+ * host-pinned, device-mapped table: no CPU gather and no staging DMA (contrast PAPER.md:221-225,
+ * Fig. 2a). The paper's alignment optimisation (§4.5) changes the access
+ * order, never the result ("the output indices are also identically adjusted to maintain the
+ * ordering"); here every kernel variant must be bit-identical to the loop above.
+ *
+ * Layout. The table is rows x rb bytes, row-major, dense, starting at host_ptr (any alignment).
+ * idx is int64 (reading R2; the 4-B sweep table has 2^32 rows). out is n x rb bytes,
+ * row-major, dense, in device memory (any alignment; 16-B aligned is the fast path).
+ *
+ * Errors. Functions return UT_OK (0) or a negative ut_status; ut_register returns NULL on
+ * failure. The reason of the last failure on the calling thread is in ut_last_error().
+ * An out-of-range or negative idx[i] is NOT a synchronous error (the kernel is asynchronous):
+ * that output row is zero-filled and the smallest such position i is recorded in a
+ * per-table, per-device error word that ut_error_pos() reads and clears (DESIGN.md reading
+ * R4, following SPEC.md:151 "index error naming the offending position").
+ *
+ * Threading. Concurrent ut_gather calls on one table from any thread, stream or device are
+ * safe (the table is read-only). ut_release must not race with in-flight gathers.
+ */
+#ifndef UT_H
+#define UT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Opaque, process-local handle of one registered table. */
+typedef struct ut_table ut_table;
+
+/* Same type as cudaStream_t (`struct CUstream_st*`); NULL = the legacy default stream. */
+typedef struct CUstream_st* ut_stream_t;
+
+typedef enum ut_status {
+  UT_OK = 0,
+  UT_EINVAL = -1,   /* bad argument: NULL pointer, zero size, overflow, unknown plan name     */
+  UT_ENOMEM = -2,   /* host registration or device scratch allocation failed                */
+  UT_ECUDA = -3,    /* a CUDA runtime call or kernel launch failed (message has the reason)  */
+  UT_ERANGE = -4,   /* ut_error_pos only: an out-of-range index was recorded                 */
+  UT_ENOTSUP = -5   /* the device cannot map host memory                                     */
+} ut_status;
+
+/*
+ * ut_register — make `rows * row_bytes` bytes at host_ptr GPU-addressable in place.
+ * The paper's `features = dataload().to("unified")` (Listing 2 line 2; Table 1
+ * PAPER.md:373) copies into a new unified allocation (§4.4); this entry
+ * instead pins and maps the caller's memory WITHOUT copying, so that several processes can
+ * register one shared table (reading R1).
+ *   host_ptr   caller-owned host memory, any alignment. It must stay valid, and unmodified while
+ *              any gather is in flight, until ut_release. If it is already page-locked and mapped
+ *              (cudaHostAlloc/cudaHostRegister by the caller), it is adopted and left pinned on
+ *              release; otherwise it is registered with cudaHostRegister(Portable|Mapped
+ *              [|ReadOnly when the device supports it]) and unregistered by ut_release.
+ *   rows       number of rows, >= 1.
+ *   row_bytes  bytes per row, >= 1; rows * row_bytes must not overflow 64 bits.
+ * The current CUDA device is used for registration; the mapping is Portable, so the handle
+ * serves every device of the process. Returns NULL on failure (UT_EINVAL / UT_ENOMEM /
+ * UT_ECUDA / UT_ENOTSUP via ut_last_error).
+ */
+ut_table* ut_register(const void* host_ptr, uint64_t rows, uint64_t row_bytes);
+
+/*
+ * ut_gather — out_dev[i*rb .. (i+1)*rb) = row idx_dev[i] of the table, for i in [0, n).
+ * The paper's `input_features = features[neighbor_id]` with a GPU index
+ * tensor and a GPU output.
+ *   t        handle from ut_register.
+ *   idx_dev  n int64 row ids in device memory of the CURRENT device (caller-owned, read-only).
+ *   n        number of rows to gather; n == 0 returns UT_OK without launching anything and
+ *            leaves out_dev untouched.
+ *   out_dev  >= n*rb bytes of device memory on the current device, not overlapping idx_dev
+ *            (caller-owned). Any alignment.
+ *   stream   stream to enqueue on; the call is asynchronous and stream-ordered, so a consumer
+ *            kernel on the same stream sees the rows.
+ * Reads touch only table bytes in [host_ptr, host_ptr + rows*rb) (reading R8).
+ * Returns UT_OK, UT_EINVAL (NULL t/idx/out with n > 0, n*rb overflow) or UT_ECUDA.
+ */
+int ut_gather(const ut_table* t, const int64_t* idx_dev, uint64_t n, void* out_dev,
+              ut_stream_t stream);
+
+/*
+ * ut_gather_host — the same gather from and to HOST buffers (the end-to-end form): copies
+ * idx_host to the device, gathers, and copies the rows back to out_host, pipelined in chunks
+ * on `stream` plus one library-owned copy stream so that the link's two directions overlap.
+ *   idx_host  n int64 row ids in host memory (page-locked for full speed; caller-owned).
+ *   out_host  >= n*rb bytes of host memory (page-locked for full speed; caller-owned).
+ * Device scratch (two chunks of idx and rows) is owned by the table and grown on demand.
+ * Synchronous: returns after out_host holds the result. Out-of-range handling as ut_gather.
+ * Returns UT_OK, UT_EINVAL, UT_ENOMEM or UT_ECUDA.
+ */
+int ut_gather_host(const ut_table* t, const int64_t* idx_host, uint64_t n, void* out_host,
+                   ut_stream_t stream);
+
+/*
+ * ut_release — free the handle; unregister the memory iff ut_register registered it.
+ * Frees the table's device error words and scratch. NULL is a no-op returning UT_OK.
+ * Must not be called while a gather on the table is in flight.
+ */
+int ut_release(ut_table* t);
+
+/*
+ * ut_error_pos — synchronise `stream`, then report and clear the smallest position i whose
+ * idx[i] was out of range (< 0 or >= rows) in any gather on the current device since the last
+ * call. *first_bad = -1 and UT_OK if none; *first_bad = i and UT_ERANGE otherwise.
+ */
+int ut_error_pos(const ut_table* t, ut_stream_t stream, int64_t* first_bad);
+
+/*
+ * ut_last_error — copy the calling thread's last error message (NUL-terminated, truncated to
+ * cap) into msg (may be NULL when cap == 0) and return its ut_status code.
+ */
+int ut_last_error(char* msg, size_t cap);
+
+/*
+ * ut_plan_name — name of the kernel variant ut_gather uses on this table for a 16-B aligned
+ * out_dev, e.g. "vec16.g32", "realign.g32x", "narrow4". The string is
+ * static. Returns "invalid" for NULL.
+ */
+const char* ut_plan_name(const ut_table* t);
+
+/*
+ * ut_set_plan — force a variant by name for A/B measurement ("auto" restores the automatic
+ * choice). Any variant accepted here is correct for any alignment it admits; a variant whose
+ * preconditions the table violates returns UT_EINVAL and leaves the plan unchanged.
+ * The environment variable UT_PLAN, read at ut_register, has the same effect.
+ */
+int ut_set_plan(ut_table* t, const char* name);
+
+/* Table facts recorded at registration (for tests and reports). */
+typedef struct ut_table_info {
+  uint64_t rows;
+  uint64_t row_bytes;
+  uint64_t host_addr;     /* host_ptr as an integer                                        */
+  uint64_t dev_addr;      /* device address of host_ptr on the registering device          */
+  int registered;         /* 1 if ut_register pinned the memory, 0 if it adopted it          */
+  int read_only;          /* 1 if registered with cudaHostRegisterReadOnly                   */
+  int base_mod128;        /* host_ptr mod 128                                               */
+  int device;             /* device that was current at registration                        */
+} ut_table_info;
+
+/* Fill *info. Returns UT_OK or UT_EINVAL. */
+int ut_table_get_info(const ut_table* t, ut_table_info* info);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* UT_H */

@@ -1,0 +1,175 @@
+"""Seeded synthetic inputs for the unified-tensor gather: host tables and index lists.
+
+This module holds none of the gather's arithmetic. It is the one place both sides of a parity
+check take their inputs from: the oracle (``oracle/``) and the CUDA path
+(``paper_2101_07956_b200``) never import each other, only this.
+
+* ``fill_table`` writes the self-identifying table content (``gen.c`` header).
+* ``uniform_idx`` draws uniform-with-replacement row ids (the paper's microbenchmark "uses a
+  random number generator (RNG) to generate random indices").
+* ``HostBuffer`` owns plain host memory (anonymous mmap, optional guard pages, or a shared
+  ``/dev/shm`` file for multi-process runs); registration/pinning is the library's job.
+* ``graphsage`` builds GraphSAGE-shaped minibatch index lists.
+"""
+from __future__ import annotations
+
+import ctypes
+import mmap
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "gen.c")
+_SO = os.path.join(_HERE, "libutgen.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile gen.c into workloads/libutgen.so (gcc, OpenMP)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        tmp = _SO + f".tmp{os.getpid()}"
+        subprocess.run(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-Wall", "-o", tmp, _SRC],
+                       check=True)
+        os.replace(tmp, _SO)
+    return _SO
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(build())
+        L.gen_splitmix64.restype = ctypes.c_uint64
+        L.gen_splitmix64.argtypes = [ctypes.c_uint64]
+        L.gen_fill_table.restype = None
+        L.gen_fill_table.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                                     ctypes.c_uint64, ctypes.c_int]
+        L.gen_uniform_idx.restype = None
+        L.gen_uniform_idx.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                                      ctypes.c_uint64]
+        L.gen_map.restype = ctypes.c_void_p
+        L.gen_map.argtypes = [ctypes.c_uint64, ctypes.c_int]
+        L.gen_unmap.restype = ctypes.c_int
+        L.gen_unmap.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
+        L.gen_map_guarded.restype = ctypes.c_void_p
+        L.gen_map_guarded.argtypes = [ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p),
+                                      ctypes.POINTER(ctypes.c_uint64)]
+        _lib = L
+    return _lib
+
+
+def splitmix64(x: int) -> int:
+    return int(lib().gen_splitmix64(x & 0xFFFFFFFFFFFFFFFF))
+
+
+def _addr(a) -> int:
+    if isinstance(a, int):
+        return a
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    raise TypeError(type(a))
+
+
+def fill_table(dst, rows: int, rb: int, seed: int, threads: int = 0) -> None:
+    """Write the self-identifying content of a rows x rb table at ``dst`` (array or address)."""
+    if isinstance(dst, np.ndarray):
+        assert dst.nbytes >= rows * rb
+    lib().gen_fill_table(_addr(dst), rows, rb, seed & 0xFFFFFFFFFFFFFFFF, threads)
+
+
+def uniform_idx(n: int, rows: int, seed: int) -> np.ndarray:
+    """n row ids uniform with replacement over [0, rows) (int64)."""
+    out = np.empty(n, dtype=np.int64)
+    if n:
+        lib().gen_uniform_idx(out.ctypes.data, n, rows, seed & 0xFFFFFFFFFFFFFFFF)
+    return out
+
+
+def decode_row_ids(rows_bytes: np.ndarray, rb: int) -> np.ndarray:
+    """Row id encoded in the first min(rb, 8) bytes of each row of a self-identifying table.
+
+    For rb < 8 only the low 8*rb bits of the id survive; callers compare modulo 2**(8*rb)."""
+    a = np.asarray(rows_bytes, dtype=np.uint8).reshape(-1, rb)
+    k = min(rb, 8)
+    pad = np.zeros((a.shape[0], 8), dtype=np.uint8)
+    pad[:, :k] = a[:, :k]
+    return pad.view("<u8").reshape(-1).astype(np.int64)
+
+
+class HostBuffer:
+    """Plain (unpinned) host memory holding a table, placed at a chosen alignment.
+
+    kind="anon":    anonymous mmap (THP-advised); the table starts ``offset`` bytes into it.
+    kind="guarded": PROT_NONE pages on both sides and the table's last byte is the last byte
+                    before the trailing guard page, so any over-read faults.
+    kind="shm":     a MAP_SHARED ``/dev/shm`` file (``name``) that several processes map;
+                    ``create`` decides who sizes it.
+    """
+
+    def __init__(self, nbytes: int, kind: str = "anon", offset: int = 0, hugepage: bool = True,
+                 name: str | None = None, create: bool = True):
+        self.nbytes = int(nbytes)
+        self.kind = kind
+        self._mm = None
+        self._fd = None
+        self._map_base = None
+        self._map_len = 0
+        self.path = None
+        if kind == "anon":
+            self._map_len = self.nbytes + offset + 4096
+            base = lib().gen_map(self._map_len, 1 if hugepage else 0)
+            if not base:
+                raise MemoryError(f"mmap of {self._map_len} bytes failed")
+            self._map_base = base
+            self.addr = base + offset
+        elif kind == "guarded":
+            mb = ctypes.c_void_p()
+            ml = ctypes.c_uint64()
+            p = lib().gen_map_guarded(self.nbytes, ctypes.byref(mb), ctypes.byref(ml))
+            if not p:
+                raise MemoryError("guarded mmap failed")
+            self._map_base = mb.value
+            self._map_len = ml.value
+            self.addr = p
+        elif kind == "shm":
+            assert name, "shm buffers need a name"
+            self.path = os.path.join("/dev/shm", name)
+            flags = os.O_RDWR | (os.O_CREAT if create else 0)
+            self._fd = os.open(self.path, flags, 0o600)
+            length = self.nbytes + offset
+            if create:
+                os.ftruncate(self._fd, length)
+            self._mm = mmap.mmap(self._fd, length, mmap.MAP_SHARED,
+                                 mmap.PROT_READ | mmap.PROT_WRITE)
+            base = ctypes.addressof(ctypes.c_char.from_buffer(self._mm))
+            self.addr = base + offset
+        else:
+            raise ValueError(kind)
+
+    def array(self) -> np.ndarray:
+        """uint8 numpy view of the table bytes (no copy)."""
+        buf = (ctypes.c_uint8 * self.nbytes).from_address(self.addr)
+        return np.ctypeslib.as_array(buf)
+
+    def close(self, unlink: bool = False) -> None:
+        if self._map_base is not None:
+            lib().gen_unmap(self._map_base, self._map_len)
+            self._map_base = None
+        if self._mm is not None:
+            try:
+                self._mm.close()
+            except BufferError:
+                pass  # a numpy view is still alive; the mapping goes with the process
+            self._mm = None
+        if self._fd is not None:
+            os.close(self._fd)
+            self._fd = None
+        if unlink and self.path and os.path.exists(self.path):
+            os.unlink(self.path)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,101 @@
+/*
+ * workloads/gen.c — seeded synthetic INPUT generators (no gather arithmetic).
+ *
+ * Shared by the tests, the oracle side and the CUDA side as the source of inputs only: it
+ * fills the host feature table and draws uniform index lists. It computes nothing the gather
+ * computes (no row addressing of an index list, no copying of rows by index).
+ *
+ * Recipe:
+ *   splitmix64(x): the standard SplitMix64 finaliser.
+ *   Table content ("self-identifying"): byte b of row r is byte (b mod 8) of
+ *       splitmix64(seed ^ (r * PHI + b / 8)),
+ *   except that the first min(rb, 8) bytes of row r are r's little-endian bytes, so that any
+ *   fetched row decodes to the row id it came from and no two rows are equal.
+ *   Uniform indices: idx[i] = floor(splitmix64(seed ^ (i * PHI)) * rows / 2^64)
+ *   (uniform with replacement over [0, rows), reading R9).
+ */
+#include <stdint.h>
+#include <string.h>
+#include <omp.h>
+
+#define PHI 0x9E3779B97F4A7C15ull
+
+static inline uint64_t splitmix64(uint64_t x)
+{
+    uint64_t z = x + PHI;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+uint64_t gen_splitmix64(uint64_t x) { return splitmix64(x); }
+
+/* Fill rows*rb bytes at dst with the self-identifying content. Rows are independent, so the
+ * loop is split over `threads` OpenMP threads (threads <= 0: all available). */
+void gen_fill_table(uint8_t* dst, uint64_t rows, uint64_t rb, uint64_t seed, int threads)
+{
+    int64_t R = (int64_t)rows;
+    int nt = threads > 0 ? threads : omp_get_max_threads();
+#pragma omp parallel for schedule(static, 4096) num_threads(nt)
+    for (int64_t r = 0; r < R; ++r) {
+        uint8_t* row = dst + (uint64_t)r * rb;
+        uint64_t base = (uint64_t)r * PHI;
+        uint64_t b = 0;
+        for (; b + 8 <= rb; b += 8) {
+            uint64_t w = splitmix64(seed ^ (base + b / 8));
+            memcpy(row + b, &w, 8);
+        }
+        if (b < rb) {
+            uint64_t w = splitmix64(seed ^ (base + b / 8));
+            memcpy(row + b, &w, rb - b);
+        }
+        uint64_t id = (uint64_t)r;
+        memcpy(row, &id, rb < 8 ? rb : 8);
+    }
+}
+
+/* idx[i] = floor(splitmix64(seed ^ (i*PHI)) * rows / 2^64), i in [0, n). */
+void gen_uniform_idx(int64_t* idx, uint64_t n, uint64_t rows, uint64_t seed)
+{
+    for (uint64_t i = 0; i < n; ++i) {
+        __uint128_t p = (__uint128_t)splitmix64(seed ^ (i * PHI)) * rows;
+        idx[i] = (int64_t)(uint64_t)(p >> 64);
+    }
+}
+
+/* ---- host memory for tables (plain mmap; the library under test pins it itself) ---------- */
+#include <sys/mman.h>
+#include <unistd.h>
+
+/* Anonymous private mapping of `bytes`, transparent-hugepage advised when hugepage != 0.
+ * Returns NULL on failure. */
+void* gen_map(uint64_t bytes, int hugepage)
+{
+    void* p = mmap(NULL, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) return NULL;
+#ifdef MADV_HUGEPAGE
+    if (hugepage) madvise(p, bytes, MADV_HUGEPAGE);
+#endif
+    return p;
+}
+
+int gen_unmap(void* p, uint64_t bytes) { return munmap(p, bytes); }
+
+/* Guard-page layout for over-read tests: [PROT_NONE page][data pages][PROT_NONE page], with the
+ * returned pointer placed so that `bytes` end exactly at the start of the trailing guard page.
+ * *map_base / *map_len describe the whole mapping for gen_unmap. */
+void* gen_map_guarded(uint64_t bytes, void** map_base, uint64_t* map_len)
+{
+    uint64_t pg = (uint64_t)sysconf(_SC_PAGESIZE);
+    uint64_t data = (bytes + pg - 1) / pg * pg;
+    uint64_t len = data + 2 * pg;
+    uint8_t* p = (uint8_t*)mmap(NULL, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) return NULL;
+    if (mprotect(p, pg, PROT_NONE) != 0 || mprotect(p + pg + data, pg, PROT_NONE) != 0) {
+        munmap(p, len);
+        return NULL;
+    }
+    *map_base = p;
+    *map_len = len;
+    return p + pg + data - bytes;
+}
