@@ -37,6 +37,12 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#define UT_API __attribute__((visibility("default")))
+#else
+#define UT_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -73,7 +79,7 @@ typedef enum ut_status {
  * serves every device of the process. Returns NULL on failure (UT_EINVAL / UT_ENOMEM /
  * UT_ECUDA / UT_ENOTSUP via ut_last_error).
  */
-ut_table* ut_register(const void* host_ptr, uint64_t rows, uint64_t row_bytes);
+UT_API ut_table* ut_register(const void* host_ptr, uint64_t rows, uint64_t row_bytes);
 
 /*
  * ut_gather — out_dev[i*rb .. (i+1)*rb) = row idx_dev[i] of the table, for i in [0, n).
@@ -90,7 +96,7 @@ ut_table* ut_register(const void* host_ptr, uint64_t rows, uint64_t row_bytes);
  * Reads touch only table bytes in [host_ptr, host_ptr + rows*rb) (reading R8).
  * Returns UT_OK, UT_EINVAL (NULL t/idx/out with n > 0, n*rb overflow) or UT_ECUDA.
  */
-int ut_gather(const ut_table* t, const int64_t* idx_dev, uint64_t n, void* out_dev,
+UT_API int ut_gather(const ut_table* t, const int64_t* idx_dev, uint64_t n, void* out_dev,
               ut_stream_t stream);
 
 /*
@@ -103,7 +109,7 @@ int ut_gather(const ut_table* t, const int64_t* idx_dev, uint64_t n, void* out_d
  * Synchronous: returns after out_host holds the result. Out-of-range handling as ut_gather.
  * Returns UT_OK, UT_EINVAL, UT_ENOMEM or UT_ECUDA.
  */
-int ut_gather_host(const ut_table* t, const int64_t* idx_host, uint64_t n, void* out_host,
+UT_API int ut_gather_host(const ut_table* t, const int64_t* idx_host, uint64_t n, void* out_host,
                    ut_stream_t stream);
 
 /*
@@ -111,27 +117,34 @@ int ut_gather_host(const ut_table* t, const int64_t* idx_host, uint64_t n, void*
  * Frees the table's device error words and scratch. NULL is a no-op returning UT_OK.
  * Must not be called while a gather on the table is in flight.
  */
-int ut_release(ut_table* t);
+UT_API int ut_release(ut_table* t);
 
 /*
  * ut_error_pos — synchronise `stream`, then report and clear the smallest position i whose
  * idx[i] was out of range (< 0 or >= rows) in any gather on the current device since the last
  * call. *first_bad = -1 and UT_OK if none; *first_bad = i and UT_ERANGE otherwise.
  */
-int ut_error_pos(const ut_table* t, ut_stream_t stream, int64_t* first_bad);
+UT_API int ut_error_pos(const ut_table* t, ut_stream_t stream, int64_t* first_bad);
 
 /*
  * ut_last_error — copy the calling thread's last error message (NUL-terminated, truncated to
  * cap) into msg (may be NULL when cap == 0) and return its ut_status code.
  */
-int ut_last_error(char* msg, size_t cap);
+UT_API int ut_last_error(char* msg, size_t cap);
 
 /*
  * ut_plan_name — name of the kernel variant ut_gather uses on this table for a 16-B aligned
  * out_dev, e.g. "vec16.g32", "realign.g32x", "narrow4". The string is
  * static. Returns "invalid" for NULL.
  */
-const char* ut_plan_name(const ut_table* t);
+UT_API const char* ut_plan_name(const ut_table* t);
+
+/*
+ * ut_plan_probe — the variant ut_gather would pick for a table at host address `base` with
+ * `rows` x `row_bytes` and an output at device address `out` (no CUDA call; for tests and
+ * reports). Returns the static plan name, or "invalid" for zero sizes.
+ */
+UT_API const char* ut_plan_probe(uint64_t base, uint64_t rows, uint64_t row_bytes, uint64_t out);
 
 /*
  * ut_set_plan — force a variant by name for A/B measurement ("auto" restores the automatic
@@ -139,7 +152,7 @@ const char* ut_plan_name(const ut_table* t);
  * preconditions the table violates returns UT_EINVAL and leaves the plan unchanged.
  * The environment variable UT_PLAN, read at ut_register, has the same effect.
  */
-int ut_set_plan(ut_table* t, const char* name);
+UT_API int ut_set_plan(ut_table* t, const char* name);
 
 /* Table facts recorded at registration (for tests and reports). */
 typedef struct ut_table_info {
@@ -154,7 +167,7 @@ typedef struct ut_table_info {
 } ut_table_info;
 
 /* Fill *info. Returns UT_OK or UT_EINVAL. */
-int ut_table_get_info(const ut_table* t, ut_table_info* info);
+UT_API int ut_table_get_info(const ut_table* t, ut_table_info* info);
 
 #ifdef __cplusplus
 }

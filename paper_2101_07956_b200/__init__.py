@@ -1,0 +1,232 @@
+"""B200-native unified-tensor gather (PyTorch-Direct, arXiv 2101.07956): Python binding.
+
+Argument marshalling over the C ABI in ``include/ut.h`` (``libut.so``, built in-tree from
+``csrc/``); every step of the gather runs in the library's sm_100a kernels. PyTorch supplies
+device memory and streams only. There is no CPU fallback: if ``libut.so`` cannot be built or
+loaded, importing the binding raises.
+
+Low level (same names and arguments as the C ABI, raw addresses and ints):
+    ut_register(host_addr, rows, row_bytes) -> handle
+    ut_gather(handle, idx_dev_addr, n, out_dev_addr, stream_handle)
+    ut_gather_host(handle, idx_host_addr, n, out_host_addr, stream_handle)
+    ut_release(handle), ut_error_pos(handle, stream_handle) -> int,
+    ut_plan_name(handle), ut_set_plan(handle, name), ut_plan_probe(base, rows, rb, out),
+    ut_table_get_info(handle) -> dict
+
+High level: ``Table`` — the paper's unified tensor, ``Table(features)[gpu_idx]`` being
+``unified_tensor[gpu_tensor]``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import _build
+
+UT_OK, UT_EINVAL, UT_ENOMEM, UT_ECUDA, UT_ERANGE, UT_ENOTSUP = 0, -1, -2, -3, -4, -5
+
+# Every symbol include/ut.h declares (tests check the library exports exactly these).
+ABI = ("ut_register", "ut_gather", "ut_gather_host", "ut_release", "ut_error_pos",
+       "ut_last_error", "ut_plan_name", "ut_plan_probe", "ut_set_plan", "ut_table_get_info")
+
+
+class UTError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("rows", ctypes.c_uint64), ("row_bytes", ctypes.c_uint64),
+                ("host_addr", ctypes.c_uint64), ("dev_addr", ctypes.c_uint64),
+                ("registered", ctypes.c_int), ("read_only", ctypes.c_int),
+                ("base_mod128", ctypes.c_int), ("device", ctypes.c_int)]
+
+
+def _load():
+    path = _build.build()          # no-op when libut.so is up to date
+    L = ctypes.CDLL(path)
+    vp, u64, i64p = ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int64)
+    L.ut_register.restype = vp
+    L.ut_register.argtypes = [vp, u64, u64]
+    L.ut_gather.restype = ctypes.c_int
+    L.ut_gather.argtypes = [vp, vp, u64, vp, vp]
+    L.ut_gather_host.restype = ctypes.c_int
+    L.ut_gather_host.argtypes = [vp, vp, u64, vp, vp]
+    L.ut_release.restype = ctypes.c_int
+    L.ut_release.argtypes = [vp]
+    L.ut_error_pos.restype = ctypes.c_int
+    L.ut_error_pos.argtypes = [vp, vp, i64p]
+    L.ut_last_error.restype = ctypes.c_int
+    L.ut_last_error.argtypes = [ctypes.c_char_p, ctypes.c_size_t]
+    L.ut_plan_name.restype = ctypes.c_char_p
+    L.ut_plan_name.argtypes = [vp]
+    L.ut_plan_probe.restype = ctypes.c_char_p
+    L.ut_plan_probe.argtypes = [u64, u64, u64, u64]
+    L.ut_set_plan.restype = ctypes.c_int
+    L.ut_set_plan.argtypes = [vp, ctypes.c_char_p]
+    L.ut_table_get_info.restype = ctypes.c_int
+    L.ut_table_get_info.argtypes = [vp, ctypes.POINTER(_Info)]
+    return L
+
+
+_lib = _load()
+LIB_PATH = _build.LIB
+
+
+def last_error() -> tuple[int, str]:
+    buf = ctypes.create_string_buffer(512)
+    code = _lib.ut_last_error(buf, 512)
+    return code, buf.value.decode(errors="replace")
+
+
+def _check(rc: int) -> int:
+    if rc != UT_OK:
+        code, msg = last_error()
+        raise UTError(rc, msg)
+    return rc
+
+
+# ---- the C ABI, name for name ---------------------------------------------------------------
+def ut_register(host_addr: int, rows: int, row_bytes: int) -> int:
+    h = _lib.ut_register(host_addr, rows, row_bytes)
+    if not h:
+        code, msg = last_error()
+        raise UTError(code, msg)
+    return h
+
+
+def ut_gather(t: int, idx_dev: int, n: int, out_dev: int, stream: int = 0) -> None:
+    _check(_lib.ut_gather(t, idx_dev, n, out_dev, stream))
+
+
+def ut_gather_host(t: int, idx_host: int, n: int, out_host: int, stream: int = 0) -> None:
+    _check(_lib.ut_gather_host(t, idx_host, n, out_host, stream))
+
+
+def ut_release(t: int) -> None:
+    _check(_lib.ut_release(t))
+
+
+def ut_error_pos(t: int, stream: int = 0) -> int:
+    v = ctypes.c_int64(-1)
+    rc = _lib.ut_error_pos(t, stream, ctypes.byref(v))
+    if rc not in (UT_OK, UT_ERANGE):
+        _check(rc)
+    return int(v.value)
+
+
+def ut_plan_name(t: int) -> str:
+    return _lib.ut_plan_name(t).decode()
+
+
+def ut_plan_probe(base: int, rows: int, row_bytes: int, out: int = 0) -> str:
+    return _lib.ut_plan_probe(base, rows, row_bytes, out).decode()
+
+
+def ut_set_plan(t: int, name: str) -> None:
+    _check(_lib.ut_set_plan(t, name.encode()))
+
+
+def ut_table_get_info(t: int) -> dict:
+    info = _Info()
+    _check(_lib.ut_table_get_info(t, ctypes.byref(info)))
+    return {k: getattr(info, k) for k, _ in _Info._fields_}
+
+
+# ---- convenience ----------------------------------------------------------------------------
+def _stream_handle(stream) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+class Table:
+    """A host-resident feature table that GPU kernels read directly (the "unified tensor").
+
+    ``host`` is a numpy array or CPU torch tensor (any dtype; its rows are the table rows), or a
+    raw address with ``rows`` and ``row_bytes``. The memory is pinned and mapped in place by
+    ``ut_register`` (no copy) and must outlive the Table."""
+
+    def __init__(self, host, rows: int | None = None, row_bytes: int | None = None):
+        self._keep = host
+        if isinstance(host, int):
+            assert rows is not None and row_bytes is not None
+            addr = host
+        else:
+            if hasattr(host, "data_ptr"):        # torch tensor
+                assert not host.is_cuda and host.is_contiguous()
+                addr = host.data_ptr()
+                nbytes = host.numel() * host.element_size()
+                shape = tuple(host.shape)
+            else:                                 # numpy
+                assert host.flags.c_contiguous
+                addr = host.ctypes.data
+                nbytes = host.nbytes
+                shape = host.shape
+            if rows is None:
+                rows = shape[0] if len(shape) > 1 else nbytes
+            if row_bytes is None:
+                row_bytes = nbytes // rows
+        self.rows, self.row_bytes, self.host_addr = int(rows), int(row_bytes), int(addr)
+        self.handle = ut_register(self.host_addr, self.rows, self.row_bytes)
+
+    @property
+    def plan(self) -> str:
+        return ut_plan_name(self.handle)
+
+    def set_plan(self, name: str) -> None:
+        ut_set_plan(self.handle, name)
+
+    def info(self) -> dict:
+        return ut_table_get_info(self.handle)
+
+    def gather(self, idx, out=None, stream=None):
+        """out[i] = row idx[i] (uint8 [n, row_bytes] CUDA tensor); idx: CUDA int64 tensor."""
+        import torch
+        assert idx.is_cuda and idx.dtype == torch.int64 and idx.is_contiguous()
+        n = idx.numel()
+        if out is None:
+            out = torch.empty((n, self.row_bytes), dtype=torch.uint8, device=idx.device)
+        else:
+            assert out.is_cuda and out.is_contiguous()
+            assert out.numel() * out.element_size() >= n * self.row_bytes
+        ut_gather(self.handle, idx.data_ptr(), n, out.data_ptr(), _stream_handle(stream))
+        return out
+
+    __getitem__ = gather
+
+    def gather_host(self, idx_host, out_host=None, stream=None):
+        """End-to-end form: host int64 idx in, host rows out (uint8 [n, row_bytes])."""
+        import torch
+        if not hasattr(idx_host, "data_ptr"):
+            idx_host = torch.from_numpy(idx_host)
+        assert not idx_host.is_cuda and idx_host.dtype == torch.int64 and idx_host.is_contiguous()
+        n = idx_host.numel()
+        if out_host is None:
+            out_host = torch.empty((n, self.row_bytes), dtype=torch.uint8, pin_memory=True)
+        ut_gather_host(self.handle, idx_host.data_ptr(), n, out_host.data_ptr(),
+                       _stream_handle(stream))
+        return out_host
+
+    def error_pos(self, stream=None) -> int:
+        """First out-of-range position since the last call (syncs the stream), or -1."""
+        return ut_error_pos(self.handle, _stream_handle(stream))
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            ut_release(self.handle)
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,538 @@
+// ut.cu — registration layer, plan selection and C ABI of the unified-tensor gather.
+//
+// Implements include/ut.h. The "unified tensor" of PyTorch-Direct is host memory that GPU
+// threads dereference directly; here the caller's table is pinned
+// and mapped in place (cudaHostRegister Portable|Mapped[|ReadOnly]) instead of copied into a new
+// allocation (reading R1), and `unified_tensor[gpu_tensor]`
+// is ut_gather. The kernels are in ut_kernels.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <unistd.h>
+
+#include "ut.h"
+#include "ut_kernels.cuh"
+
+namespace {
+
+constexpr int kMaxDev = 64;
+
+thread_local int g_err_code = UT_OK;
+thread_local char g_err_msg[512] = "";
+
+int set_err(int code, const char* fmt, ...) {
+  g_err_code = code;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err_msg, sizeof g_err_msg, fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_err(cudaError_t e, const char* what) {
+  return set_err(UT_ECUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+// ---- plans ------------------------------------------------------------------------------------
+enum PlanKind { P_AUTO = -1, P_NARROW = 0, P_VEC16 = 1, P_VEC16X = 2, P_REALIGN = 3, P_REALIGNX = 4 };
+
+struct Plan {
+  PlanKind kind;
+  int g;       // lanes per row (single-pass) or element bytes (narrow)
+  bool clip;   // realign: table base or end not 16-B aligned
+};
+
+const char* plan_name(const Plan& p) {
+  switch (p.kind) {
+    case P_NARROW:
+      switch (p.g) { case 1: return "narrow1"; case 2: return "narrow2"; case 4: return "narrow4";
+                     default: return "narrow8"; }
+    case P_VEC16:
+      switch (p.g) { case 1: return "vec16.g1"; case 2: return "vec16.g2"; case 4: return "vec16.g4";
+                     case 8: return "vec16.g8"; case 16: return "vec16.g16"; default: return "vec16.g32"; }
+    case P_VEC16X: return "vec16.g32x";
+    case P_REALIGN:
+      switch (p.g) { case 1: return "realign.g1"; case 2: return "realign.g2"; case 4: return "realign.g4";
+                     case 8: return "realign.g8"; case 16: return "realign.g16"; default: return "realign.g32"; }
+    case P_REALIGNX: return "realign.g32x";
+    default: return "invalid";
+  }
+}
+
+int pow2ceil(uint64_t x) {
+  int g = 1;
+  while ((uint64_t)g < x) g <<= 1;
+  return g;
+}
+
+// Largest number of 16-B chunks a row spans over the residues (start mod 16) that
+// start = a0 + k*rb can take.
+uint64_t max_span16(uint64_t a0, uint64_t rb) {
+  uint64_t m = 0;
+  for (uint64_t k = 0; k < 16; ++k) {
+    uint64_t o = (a0 + k * rb) & 15;
+    m = std::max(m, (o + rb + 15) / 16);
+  }
+  return m;
+}
+
+// The automatic choice (DESIGN.md §Plan selection), or the forced kind when it is admissible.
+bool choose_plan(uint64_t base, uint64_t rows, uint64_t rb, uint64_t out, PlanKind forced, Plan* p) {
+  const bool clip = ((base & 15) != 0) || (((base + rows * rb) & 15) != 0);
+  const bool natural = (rb == 1 || rb == 2 || rb == 4 || rb == 8) && (base % rb == 0) && (out % rb == 0);
+  const bool aligned = ((base | rb | out) & 15) == 0;
+  const uint64_t span = std::max(max_span16(base, rb), max_span16(out, rb));
+  PlanKind k = forced;
+  if (k == P_AUTO) {
+    if (natural) k = P_NARROW;
+    else if (aligned) k = rb <= 512 ? P_VEC16 : P_VEC16X;
+    else k = span <= 32 ? P_REALIGN : P_REALIGNX;
+  }
+  switch (k) {
+    case P_NARROW:
+      if (!natural) return false;
+      *p = Plan{k, (int)rb, false};
+      return true;
+    case P_VEC16:
+      if (!aligned || rb > 512) return false;
+      *p = Plan{k, pow2ceil(rb / 16), false};
+      return true;
+    case P_VEC16X:
+      if (!aligned) return false;
+      *p = Plan{k, 32, false};
+      return true;
+    case P_REALIGN:
+      if (span > 32) return false;
+      *p = Plan{k, pow2ceil(span), clip};
+      return true;
+    case P_REALIGNX:
+      *p = Plan{k, 32, clip};
+      return true;
+    default:
+      return false;
+  }
+}
+
+PlanKind parse_plan(const char* s, bool* ok) {
+  *ok = true;
+  if (!s || !strcmp(s, "auto")) return P_AUTO;
+  if (!strcmp(s, "narrow")) return P_NARROW;
+  if (!strcmp(s, "vec16")) return P_VEC16;
+  if (!strcmp(s, "vec16x")) return P_VEC16X;
+  if (!strcmp(s, "realign")) return P_REALIGN;
+  if (!strcmp(s, "realignx")) return P_REALIGNX;
+  *ok = false;
+  return P_AUTO;
+}
+
+struct DevState {
+  bool init = false;
+  uint64_t dev_base = 0;               // device address of the table on this device
+  unsigned long long* err = nullptr;   // first out-of-range position, ~0 = none
+  int sms = 0;
+  // ut_gather_host scratch
+  static constexpr int kBuf = 3;
+  int64_t* idx_buf[kBuf] = {};
+  uint8_t* out_buf[kBuf] = {};
+  uint64_t buf_rows = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t gathered[kBuf] = {};
+  cudaEvent_t drained[kBuf] = {};
+};
+
+}  // namespace
+
+struct ut_table {
+  const uint8_t* host = nullptr;
+  uint64_t rows = 0, rb = 0, bytes = 0;
+  const uint8_t* reg_base = nullptr;   // page-aligned registered range
+  uint64_t reg_len = 0;
+  int registered = 0, read_only = 0, device = 0;
+  PlanKind forced = P_AUTO;
+  std::mutex mu;
+  DevState dev[kMaxDev];
+};
+
+namespace {
+
+// Lazily resolve the table's device address and error word on the current device.
+int dev_state(const ut_table* ct, DevState** out) {
+  ut_table* t = const_cast<ut_table*>(ct);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_err(e, "cudaGetDevice");
+  if (dev < 0 || dev >= kMaxDev) return set_err(UT_ENOTSUP, "device %d beyond %d", dev, kMaxDev);
+  DevState* s = &t->dev[dev];
+  if (s->init) {
+    *out = s;
+    return UT_OK;
+  }
+  std::lock_guard<std::mutex> lk(t->mu);
+  if (!s->init) {
+    void* dp = nullptr;
+    e = cudaHostGetDevicePointer(&dp, const_cast<uint8_t*>(t->reg_base), 0);
+    if (e != cudaSuccess) return cuda_err(e, "cudaHostGetDevicePointer");
+    unsigned long long* err = nullptr;
+    e = cudaMalloc(&err, sizeof *err);
+    if (e != cudaSuccess) return cuda_err(e, "cudaMalloc(error word)");
+    e = cudaMemset(err, 0xff, sizeof *err);
+    if (e != cudaSuccess) return cuda_err(e, "cudaMemset(error word)");
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    s->dev_base = (uint64_t)dp + (uint64_t)(t->host - t->reg_base);
+    s->err = err;
+    s->sms = sms > 0 ? sms : 148;
+    s->init = true;
+  }
+  *out = s;
+  return UT_OK;
+}
+
+template <typename K>
+int grid_for(K kernel, int sms, uint64_t work_warps) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
+  if (per_sm <= 0) per_sm = 1;
+  uint64_t full = (uint64_t)sms * per_sm;
+  uint64_t need = (work_warps + 7) / 8;
+  return (int)std::max<uint64_t>(1, std::min(full, need));
+}
+
+constexpr int kU = 4;    // single-pass: row steps in flight per warp tile
+constexpr int kUx = 2;   // multi-pass: LDG.128 per lane in flight per row iteration
+constexpr int kUn = 4;   // narrow: rows per thread in flight
+
+template <typename K>
+cudaError_t launch(K kernel, int grid, cudaStream_t st, const ut::GatherArgs& a) {
+  kernel<<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int G>
+cudaError_t launch_single(const Plan& p, int sms, cudaStream_t st, const ut::GatherArgs& a) {
+  constexpr uint64_t rpt = (32 / G) * kU;
+  const uint64_t tiles = (a.n + rpt - 1) / rpt;
+  if (p.kind == P_VEC16) {
+    auto k = ut::k_single<G, kU, true, false>;
+    return launch(k, grid_for(k, sms, tiles), st, a);
+  }
+  if (p.clip) {
+    auto k = ut::k_single<G, kU, false, true>;
+    return launch(k, grid_for(k, sms, tiles), st, a);
+  }
+  auto k = ut::k_single<G, kU, false, false>;
+  return launch(k, grid_for(k, sms, tiles), st, a);
+}
+
+cudaError_t launch_plan(const Plan& p, int sms, cudaStream_t st, const ut::GatherArgs& a) {
+  switch (p.kind) {
+    case P_NARROW: {
+      const uint64_t warps = (a.n + 32 * kUn - 1) / (32 * kUn);
+      switch (p.g) {
+        case 1: { auto k = ut::k_narrow<uint8_t, kUn>; return launch(k, grid_for(k, sms, warps), st, a); }
+        case 2: { auto k = ut::k_narrow<uint16_t, kUn>; return launch(k, grid_for(k, sms, warps), st, a); }
+        case 4: { auto k = ut::k_narrow<uint32_t, kUn>; return launch(k, grid_for(k, sms, warps), st, a); }
+        default: { auto k = ut::k_narrow<uint64_t, kUn>; return launch(k, grid_for(k, sms, warps), st, a); }
+      }
+    }
+    case P_VEC16:
+    case P_REALIGN:
+      switch (p.g) {
+        case 1: return launch_single<1>(p, sms, st, a);
+        case 2: return launch_single<2>(p, sms, st, a);
+        case 4: return launch_single<4>(p, sms, st, a);
+        case 8: return launch_single<8>(p, sms, st, a);
+        case 16: return launch_single<16>(p, sms, st, a);
+        default: return launch_single<32>(p, sms, st, a);
+      }
+    case P_VEC16X: {
+      auto k = ut::k_multi<kUx, true, false>;
+      return launch(k, grid_for(k, sms, a.n), st, a);
+    }
+    case P_REALIGNX: {
+      if (p.clip) {
+        auto k = ut::k_multi<kUx, false, true>;
+        return launch(k, grid_for(k, sms, a.n), st, a);
+      }
+      auto k = ut::k_multi<kUx, false, false>;
+      return launch(k, grid_for(k, sms, a.n), st, a);
+    }
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n, void* out_dev,
+              cudaStream_t st) {
+  Plan p;
+  if (!choose_plan((uint64_t)t->host, t->rows, t->rb, (uint64_t)out_dev, t->forced, &p) &&
+      !choose_plan((uint64_t)t->host, t->rows, t->rb, (uint64_t)out_dev, P_AUTO, &p))
+    return set_err(UT_EINVAL, "no admissible plan");
+  ut::GatherArgs a{s->dev_base, t->rows, t->rb, idx_dev, n, (uint64_t)out_dev, s->err};
+  cudaError_t e = launch_plan(p, s->sms, st, a);
+  if (e != cudaSuccess) return cuda_err(e, plan_name(p));
+  return UT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ut_table* ut_register(const void* host_ptr, uint64_t rows, uint64_t row_bytes) {
+  if (!host_ptr) return set_err(UT_EINVAL, "host_ptr is NULL"), nullptr;
+  if (rows == 0 || row_bytes == 0) return set_err(UT_EINVAL, "rows and row_bytes must be >= 1"), nullptr;
+  if (rows > UINT64_MAX / row_bytes) return set_err(UT_EINVAL, "rows*row_bytes overflows"), nullptr;
+  const uint64_t bytes = rows * row_bytes;
+  if ((uint64_t)host_ptr > UINT64_MAX - bytes) return set_err(UT_EINVAL, "table wraps the address space"), nullptr;
+
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_err(e, "cudaGetDevice"), nullptr;
+  int can_map = 0;
+  cudaDeviceGetAttribute(&can_map, cudaDevAttrCanMapHostMemory, dev);
+  if (!can_map) return set_err(UT_ENOTSUP, "device %d cannot map host memory", dev), nullptr;
+
+  const uint64_t pg = (uint64_t)sysconf(_SC_PAGESIZE);
+  const uint64_t lo = (uint64_t)host_ptr / pg * pg;
+  const uint64_t hi = ((uint64_t)host_ptr + bytes + pg - 1) / pg * pg;
+
+  ut_table* t = new (std::nothrow) ut_table;
+  if (!t) return set_err(UT_ENOMEM, "out of host memory"), nullptr;
+  t->host = (const uint8_t*)host_ptr;
+  t->rows = rows;
+  t->rb = row_bytes;
+  t->bytes = bytes;
+  t->device = dev;
+
+  // Already page-locked and mapped (cudaHostAlloc / a previous registration)? Adopt it.
+  cudaPointerAttributes attr{};
+  e = cudaPointerGetAttributes(&attr, host_ptr);
+  cudaPointerAttributes attr_end{};
+  cudaError_t e2 = cudaPointerGetAttributes(&attr_end, (const uint8_t*)host_ptr + bytes - 1);
+  if (e == cudaSuccess && e2 == cudaSuccess && attr.type == cudaMemoryTypeHost &&
+      attr_end.type == cudaMemoryTypeHost && attr.devicePointer != nullptr) {
+    t->reg_base = (const uint8_t*)host_ptr;
+    t->reg_len = bytes;
+    t->registered = 0;
+  } else {
+    cudaGetLastError();
+    int ro_ok = 0;
+    cudaDeviceGetAttribute(&ro_ok, cudaDevAttrHostRegisterReadOnlySupported, dev);
+    unsigned flags = cudaHostRegisterPortable | cudaHostRegisterMapped;
+    e = cudaErrorUnknown;
+    if (ro_ok) {
+      e = cudaHostRegister((void*)lo, hi - lo, flags | cudaHostRegisterReadOnly);
+      if (e == cudaSuccess) t->read_only = 1;
+      else cudaGetLastError();
+    }
+    if (e != cudaSuccess) e = cudaHostRegister((void*)lo, hi - lo, flags);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      delete t;
+      if (e == cudaErrorMemoryAllocation)
+        return set_err(UT_ENOMEM, "cudaHostRegister(%llu bytes): %s", (unsigned long long)(hi - lo),
+                       cudaGetErrorString(e)), nullptr;
+      return cuda_err(e, "cudaHostRegister"), nullptr;
+    }
+    t->reg_base = (const uint8_t*)lo;
+    t->reg_len = hi - lo;
+    t->registered = 1;
+  }
+  const char* env = getenv("UT_PLAN");
+  if (env && *env) {
+    bool ok;
+    PlanKind k = parse_plan(env, &ok);
+    Plan p;
+    if (ok && (k == P_AUTO || choose_plan((uint64_t)t->host, rows, row_bytes, 0, k, &p))) t->forced = k;
+  }
+  DevState* s;
+  if (dev_state(t, &s) != UT_OK) {
+    char msg[512];
+    int code = ut_last_error(msg, sizeof msg);
+    ut_release(t);
+    set_err(code, "%s", msg);
+    return nullptr;
+  }
+  g_err_code = UT_OK;
+  g_err_msg[0] = 0;
+  return t;
+}
+
+int ut_gather(const ut_table* t, const int64_t* idx_dev, uint64_t n, void* out_dev, ut_stream_t stream) {
+  if (!t) return set_err(UT_EINVAL, "table is NULL");
+  if (n == 0) return UT_OK;
+  if (!idx_dev || !out_dev) return set_err(UT_EINVAL, "idx_dev/out_dev is NULL");
+  if (n > UINT64_MAX / t->rb) return set_err(UT_EINVAL, "n*row_bytes overflows");
+  DevState* s;
+  int rc = dev_state(t, &s);
+  if (rc != UT_OK) return rc;
+  return gather_on(t, s, idx_dev, n, out_dev, (cudaStream_t)stream);
+}
+
+int ut_gather_host(const ut_table* ct, const int64_t* idx_host, uint64_t n, void* out_host,
+                   ut_stream_t stream) {
+  if (!ct) return set_err(UT_EINVAL, "table is NULL");
+  if (n == 0) return UT_OK;
+  if (!idx_host || !out_host) return set_err(UT_EINVAL, "idx_host/out_host is NULL");
+  if (n > UINT64_MAX / ct->rb) return set_err(UT_EINVAL, "n*row_bytes overflows");
+  ut_table* t = const_cast<ut_table*>(ct);
+  DevState* s;
+  int rc = dev_state(t, &s);
+  if (rc != UT_OK) return rc;
+  std::lock_guard<std::mutex> lk(t->mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t chunk_bytes = 8ull << 20;
+  const uint64_t chunk = std::max<uint64_t>(1, chunk_bytes / t->rb);
+  const uint64_t want = std::min<uint64_t>(chunk, n);
+  cudaError_t e;
+  if (s->buf_rows < want) {
+    for (int b = 0; b < DevState::kBuf; ++b) {
+      cudaFree(s->idx_buf[b]);
+      cudaFree(s->out_buf[b]);
+      s->idx_buf[b] = nullptr;
+      s->out_buf[b] = nullptr;
+    }
+    s->buf_rows = 0;
+    for (int b = 0; b < DevState::kBuf; ++b) {
+      if (cudaMalloc(&s->idx_buf[b], want * sizeof(int64_t)) != cudaSuccess ||
+          cudaMalloc(&s->out_buf[b], want * t->rb) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(UT_ENOMEM, "device scratch of %llu rows", (unsigned long long)want);
+      }
+    }
+    s->buf_rows = want;
+  }
+  if (!s->copy_stream) {
+    if ((e = cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_err(e, "cudaStreamCreate");
+    for (int b = 0; b < DevState::kBuf; ++b) {
+      cudaEventCreateWithFlags(&s->gathered[b], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&s->drained[b], cudaEventDisableTiming);
+    }
+  }
+  const uint64_t per = s->buf_rows;
+  uint64_t k = 0;
+  for (uint64_t off = 0; off < n; off += per, ++k) {
+    const int b = (int)(k % DevState::kBuf);
+    const uint64_t cnt = std::min(per, n - off);
+    if (k >= DevState::kBuf) cudaStreamWaitEvent(st, s->drained[b], 0);
+    if ((e = cudaMemcpyAsync(s->idx_buf[b], idx_host + off, cnt * sizeof(int64_t),
+                             cudaMemcpyHostToDevice, st)) != cudaSuccess)
+      return cuda_err(e, "cudaMemcpyAsync(idx H2D)");
+    if ((rc = gather_on(t, s, s->idx_buf[b], cnt, s->out_buf[b], st)) != UT_OK) return rc;
+    cudaEventRecord(s->gathered[b], st);
+    cudaStreamWaitEvent(s->copy_stream, s->gathered[b], 0);
+    if ((e = cudaMemcpyAsync((uint8_t*)out_host + off * t->rb, s->out_buf[b], cnt * t->rb,
+                             cudaMemcpyDeviceToHost, s->copy_stream)) != cudaSuccess)
+      return cuda_err(e, "cudaMemcpyAsync(rows D2H)");
+    cudaEventRecord(s->drained[b], s->copy_stream);
+  }
+  if ((e = cudaStreamSynchronize(s->copy_stream)) != cudaSuccess) return cuda_err(e, "sync copy stream");
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_err(e, "sync stream");
+  return UT_OK;
+}
+
+int ut_release(ut_table* t) {
+  if (!t) return UT_OK;
+  int rc = UT_OK;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (int d = 0; d < kMaxDev; ++d) {
+    DevState& s = t->dev[d];
+    if (!s.init && !s.copy_stream && !s.buf_rows) continue;
+    cudaSetDevice(d);
+    if (s.err) cudaFree(s.err);
+    for (int b = 0; b < DevState::kBuf; ++b) {
+      if (s.idx_buf[b]) cudaFree(s.idx_buf[b]);
+      if (s.out_buf[b]) cudaFree(s.out_buf[b]);
+      if (s.gathered[b]) cudaEventDestroy(s.gathered[b]);
+      if (s.drained[b]) cudaEventDestroy(s.drained[b]);
+    }
+    if (s.copy_stream) cudaStreamDestroy(s.copy_stream);
+  }
+  cudaSetDevice(cur);
+  if (t->registered) {
+    cudaError_t e = cudaHostUnregister(const_cast<uint8_t*>(t->reg_base));
+    if (e != cudaSuccess) rc = cuda_err(e, "cudaHostUnregister");
+  }
+  delete t;
+  return rc;
+}
+
+int ut_error_pos(const ut_table* t, ut_stream_t stream, int64_t* first_bad) {
+  if (!t || !first_bad) return set_err(UT_EINVAL, "NULL argument");
+  DevState* s;
+  int rc = dev_state(t, &s);
+  if (rc != UT_OK) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long v = ~0ull;
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_err(e, "cudaStreamSynchronize");
+  e = cudaMemcpy(&v, s->err, sizeof v, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_err(e, "cudaMemcpy(error word)");
+  e = cudaMemset(s->err, 0xff, sizeof v);
+  if (e != cudaSuccess) return cuda_err(e, "cudaMemset(error word)");
+  if (v == ~0ull) {
+    *first_bad = -1;
+    return UT_OK;
+  }
+  *first_bad = (int64_t)v;
+  return UT_ERANGE;
+}
+
+int ut_last_error(char* msg, size_t cap) {
+  if (msg && cap) {
+    strncpy(msg, g_err_msg, cap - 1);
+    msg[cap - 1] = 0;
+  }
+  return g_err_code;
+}
+
+const char* ut_plan_name(const ut_table* t) {
+  if (!t) return "invalid";
+  Plan p;
+  if (!choose_plan((uint64_t)t->host, t->rows, t->rb, 0, t->forced, &p) &&
+      !choose_plan((uint64_t)t->host, t->rows, t->rb, 0, P_AUTO, &p))
+    return "invalid";
+  return plan_name(p);
+}
+
+const char* ut_plan_probe(uint64_t base, uint64_t rows, uint64_t row_bytes, uint64_t out) {
+  if (rows == 0 || row_bytes == 0 || rows > UINT64_MAX / row_bytes) return "invalid";
+  Plan p;
+  if (!choose_plan(base, rows, row_bytes, out, P_AUTO, &p)) return "invalid";
+  return plan_name(p);
+}
+
+int ut_set_plan(ut_table* t, const char* name) {
+  if (!t || !name) return set_err(UT_EINVAL, "NULL argument");
+  bool ok;
+  PlanKind k = parse_plan(name, &ok);
+  if (!ok) return set_err(UT_EINVAL, "unknown plan '%s'", name);
+  Plan p;
+  if (k != P_AUTO && !choose_plan((uint64_t)t->host, t->rows, t->rb, 0, k, &p))
+    return set_err(UT_EINVAL, "plan '%s' not admissible for this table", name);
+  t->forced = k;
+  return UT_OK;
+}
+
+int ut_table_get_info(const ut_table* t, ut_table_info* info) {
+  if (!t || !info) return set_err(UT_EINVAL, "NULL argument");
+  info->rows = t->rows;
+  info->row_bytes = t->rb;
+  info->host_addr = (uint64_t)t->host;
+  const DevState& s = t->dev[t->device];
+  info->dev_addr = s.init ? s.dev_base : 0;
+  info->registered = t->registered;
+  info->read_only = t->read_only;
+  info->base_mod128 = (int)((uint64_t)t->host & 127);
+  info->device = t->device;
+  return UT_OK;
+}
+
+}  // extern "C"

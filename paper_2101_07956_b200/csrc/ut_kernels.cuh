@@ -1,0 +1,302 @@
+// ut_kernels.cuh — sm_100a gather kernels of the unified-tensor gather (include/ut.h).
+//
+// Every kernel computes out[i*rb .. (i+1)*rb) = table[idx[i]*rb .. (idx[i]+1)*rb) for i < n,
+// reading the table through its device mapping of host memory (Fig. 2b) and
+// writing HBM. They differ only in how threads are mapped to bytes:
+//
+//   narrow<T>      rb in {1,2,4,8}, naturally aligned base and out: one thread per row, one
+//                  native-width load and store.
+//   vec16<G>       base, rb, out all 16-B aligned and rb <= 512: G lanes per row (G = pow2 >=
+//                  rb/16), one 16-B load + store per lane, U rows per group in flight.
+//   vec16x         as vec16 with rb > 512: one warp per row, the warp's 16-B windows aligned to
+//                  128-B lines (each LDG.128 instruction covers exactly 4 whole lines, the B200
+//                  form of the paper's "aligned and merged to the GPU cacheline (128-byte)
+//                  granularity"), U instructions in flight per lane.
+//   realign<G>     any alignment, rows spanning <= G 16-B chunks: lanes load the row's
+//                  16-B-aligned source chunks, exchange neighbours with __shfl_sync and funnel-
+//                  shift them onto the destination's 16-B grid (the paper's "output indices are
+//                  also identically adjusted"), 16-B stores inside the row and
+//                  narrow stores for the two partial edge chunks.
+//   realignx       any alignment, wide rows: warp per row, 128-B aligned source windows, a
+//                  one-chunk carry between iterations.
+//
+// Reads never touch table bytes outside [tbase, tend): a 16-B chunk that straddles the table's
+// first or last byte is read byte by byte (CLIP variants; only possible when the table's base or
+// end is not 16-B aligned). An index < 0 or >= rows zero-fills its row and atomicMin's its
+// position into *err (reading R4).
+#pragma once
+#include <cstdint>
+
+namespace ut {
+
+struct V4 {
+  uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ V4 v4_zero() { return V4{0u, 0u, 0u, 0u}; }
+
+// 16-B load from the device-mapped host table. Non-coherent path, no L1 allocation: the table
+// is read-only for the duration of a gather and every byte is used once per request.
+__device__ __forceinline__ V4 ld_table16(uint64_t a) {
+  V4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(a));
+  return v;
+}
+
+__device__ __forceinline__ uint32_t ld_table_u8(uint64_t a) {
+  uint16_t v;
+  asm("ld.global.nc.u8 %0, [%1];" : "=h"(v) : "l"(a));
+  return v;
+}
+
+// 16-B chunk at a (16-B aligned) of which only the bytes in [lo, hi) may be read; the rest are 0.
+__device__ __noinline__ V4 ld_table16_clipped(uint64_t a, uint64_t lo, uint64_t hi) {
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int b = 0; b < 16; ++b) {
+    uint64_t p = a + b;
+    if (p >= lo && p < hi) w[b >> 2] |= ld_table_u8(p) << ((b & 3) * 8);
+  }
+  return V4{w[0], w[1], w[2], w[3]};
+}
+
+template <bool CLIP>
+__device__ __forceinline__ V4 ld_chunk(uint64_t a, uint64_t tbase, uint64_t tend) {
+  if (CLIP && (a < tbase || a + 16 > tend)) return ld_table16_clipped(a, tbase, tend);
+  return ld_table16(a);
+}
+
+__device__ __forceinline__ void st16(uint64_t a, V4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(a), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// Store bytes [lo, hi) of the 16-B value v to the 16-B aligned address D (+lo), using the widest
+// naturally aligned pieces. Only the two edge chunks of a row take this path.
+__device__ __noinline__ void st_partial(uint64_t D, V4 v, int lo, int hi) {
+  uint64_t w0 = (uint64_t)v.x | ((uint64_t)v.y << 32);
+  uint64_t w1 = (uint64_t)v.z | ((uint64_t)v.w << 32);
+  int b = lo;
+  while (b < hi) {
+    uint64_t w = b < 8 ? w0 : w1;
+    int sh = (b & 7) * 8;
+    if ((b & 7) == 0 && hi - b >= 8) {
+      *reinterpret_cast<uint64_t*>(D + b) = w;
+      b += 8;
+    } else if ((b & 3) == 0 && hi - b >= 4) {
+      *reinterpret_cast<uint32_t*>(D + b) = (uint32_t)(w >> sh);
+      b += 4;
+    } else if ((b & 1) == 0 && hi - b >= 2) {
+      *reinterpret_cast<uint16_t*>(D + b) = (uint16_t)(w >> sh);
+      b += 2;
+    } else {
+      *reinterpret_cast<uint8_t*>(D + b) = (uint8_t)(w >> sh);
+      b += 1;
+    }
+  }
+}
+
+// Store the part of the 16-B destination chunk at D (16-B aligned) that lies in [d, dend).
+__device__ __forceinline__ void st_chunk_clip(uint64_t D, V4 v, uint64_t d, uint64_t dend) {
+  if (D >= d && D + 16 <= dend) {
+    st16(D, v);
+  } else if (D + 16 > d && D < dend) {
+    int lo = D < d ? (int)(d - D) : 0;
+    int hi = D + 16 > dend ? (int)(dend - D) : 16;
+    st_partial(D, v, lo, hi);
+  }
+}
+
+// Bytes [r, r+16) of the 32-byte little-endian concatenation lo || hi, r in [0, 16).
+__device__ __forceinline__ V4 funnel16(V4 lo, V4 hi, int r) {
+  const int q = r >> 2;
+  const uint32_t sh = (uint32_t)(r & 3) * 8u;
+  uint32_t t0 = q == 0 ? lo.x : q == 1 ? lo.y : q == 2 ? lo.z : lo.w;
+  uint32_t t1 = q == 0 ? lo.y : q == 1 ? lo.z : q == 2 ? lo.w : hi.x;
+  uint32_t t2 = q == 0 ? lo.z : q == 1 ? lo.w : q == 2 ? hi.x : hi.y;
+  uint32_t t3 = q == 0 ? lo.w : q == 1 ? hi.x : q == 2 ? hi.y : hi.z;
+  uint32_t t4 = q == 0 ? hi.x : q == 1 ? hi.y : q == 2 ? hi.z : hi.w;
+  return V4{__funnelshift_r(t0, t1, sh), __funnelshift_r(t1, t2, sh), __funnelshift_r(t2, t3, sh),
+            __funnelshift_r(t3, t4, sh)};
+}
+
+__device__ __forceinline__ V4 shfl4(V4 v, int src, int width) {
+  return V4{__shfl_sync(0xffffffffu, v.x, src, width), __shfl_sync(0xffffffffu, v.y, src, width),
+            __shfl_sync(0xffffffffu, v.z, src, width), __shfl_sync(0xffffffffu, v.w, src, width)};
+}
+
+__device__ __forceinline__ V4 shfl4_up1(V4 v) {
+  return V4{__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1),
+            __shfl_up_sync(0xffffffffu, v.z, 1), __shfl_up_sync(0xffffffffu, v.w, 1)};
+}
+
+struct GatherArgs {
+  uint64_t tbase;   // device address of table byte 0
+  uint64_t rows;
+  uint64_t rb;
+  const int64_t* idx;
+  uint64_t n;
+  uint64_t out;     // device address of out byte 0
+  unsigned long long* err;
+};
+
+__device__ __forceinline__ void record_bad(unsigned long long* err, uint64_t i) {
+  atomicMin(err, (unsigned long long)i);
+}
+
+// ---------------------------------------------------------------------------------------------
+// narrow<T>: one thread per row, U rows per thread in flight.
+template <typename T, int U>
+__global__ void __launch_bounds__(256) k_narrow(GatherArgs a) {
+  const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint64_t base = 0; base < a.n; base += nthreads * U) {
+    T v[U];
+    bool inb[U], ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      uint64_t i = base + (uint64_t)u * nthreads + t0;
+      inb[u] = i < a.n;
+      int64_t r = inb[u] ? __ldg(a.idx + i) : 0;
+      ok[u] = inb[u] && (uint64_t)r < a.rows;
+      v[u] = ok[u] ? *reinterpret_cast<const T*>(a.tbase + (uint64_t)r * sizeof(T)) : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      uint64_t i = base + (uint64_t)u * nthreads + t0;
+      if (inb[u]) {
+        *reinterpret_cast<T*>(a.out + i * sizeof(T)) = v[u];
+        if (!ok[u]) record_bad(a.err, i);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Single-pass kernels: G lanes per row, 32/G rows per warp step, U steps in flight per warp tile.
+// ALIGNED: base, rb, out 16-B aligned (vec16<G>); else realign<G>.
+template <int G, int U, bool ALIGNED, bool CLIP>
+__global__ void __launch_bounds__(256) k_single(GatherArgs a) {
+  constexpr int RPS = 32 / G;          // rows per warp step
+  constexpr int RPT = RPS * U;         // rows per warp tile
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / G;
+  const int q = lane % G;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t ntiles = (a.n + RPT - 1) / RPT;
+  const uint64_t tend = a.tbase + a.rows * a.rb;
+
+  for (uint64_t tile = warp; tile < ntiles; tile += nwarps) {
+    V4 cur[U];
+    uint64_t s[U];
+    bool inb[U], ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = tile * RPT + (uint64_t)u * RPS + grp;
+      inb[u] = i < a.n;
+      const int64_t r = inb[u] ? __ldg(a.idx + i) : 0;
+      ok[u] = inb[u] && (uint64_t)r < a.rows;
+      s[u] = a.tbase + (ok[u] ? (uint64_t)r : 0ull) * a.rb;
+      cur[u] = v4_zero();
+      if (ALIGNED) {
+        if (ok[u] && (uint64_t)q * 16 < a.rb) cur[u] = ld_table16(s[u] + 16ull * q);
+      } else {
+        const uint64_t s0 = s[u] & ~15ull;
+        const uint64_t A = s0 + 16ull * q;
+        if (ok[u] && A < s[u] + a.rb) cur[u] = ld_chunk<CLIP>(A, a.tbase, tend);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = tile * RPT + (uint64_t)u * RPS + grp;
+      const uint64_t d = a.out + i * a.rb;
+      if (ALIGNED) {
+        if (inb[u] && (uint64_t)q * 16 < a.rb) st16(d + 16ull * q, cur[u]);
+      } else {
+        // destination chunk q of the row sits at D = floor16(d) + 16q; its source bytes start
+        // at D + (s - d), i.e. chunk q+koff of the source window at byte offset r.
+        const int delta = (int)(s[u] & 15) - (int)(d & 15);
+        const int koff = delta < 0 ? -1 : 0;
+        const int r = delta & 15;
+        const int k = q + koff;
+        V4 lo = shfl4(cur[u], k & (G - 1), G);
+        V4 hi = shfl4(cur[u], (k + 1) & (G - 1), G);
+        if (k < 0) lo = v4_zero();
+        if (k + 1 >= G) hi = v4_zero();
+        if (inb[u]) {
+          const uint64_t D = (d & ~15ull) + 16ull * q;
+          st_chunk_clip(D, funnel16(lo, hi, r), d, d + a.rb);
+        }
+      }
+      if (inb[u] && !ok[u] && q == 0) record_bad(a.err, i);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Multi-pass kernels: one warp per row, the row's source window starts on a 128-B line and is
+// walked 32*U chunks at a time (U LDG.128 per lane in flight).
+template <int U, bool ALIGNED, bool CLIP>
+__global__ void __launch_bounds__(256) k_multi(GatherArgs a) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t tend = a.tbase + a.rows * a.rb;
+
+  for (uint64_t i = warp; i < a.n; i += nwarps) {
+    const int64_t ridx = __ldg(a.idx + i);
+    const bool ok = (uint64_t)ridx < a.rows;
+    const uint64_t s = a.tbase + (ok ? (uint64_t)ridx : 0ull) * a.rb;
+    const uint64_t send = s + a.rb;
+    const uint64_t d = a.out + i * a.rb;
+    const uint64_t ws = s & ~127ull;
+    const uint64_t we = (send + 15) & ~15ull;
+    const uint64_t nch = (we - ws) >> 4;
+    if (ALIGNED) {
+      for (uint64_t c0 = 0; c0 < nch; c0 += 32 * U) {
+        V4 cur[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint64_t A = ws + 16ull * (c0 + 32u * u + lane);
+          cur[u] = (ok && A >= s && A < send) ? ld_table16(A) : v4_zero();
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint64_t A = ws + 16ull * (c0 + 32u * u + lane);
+          if (A >= s && A < send) st16(A - s + d, cur[u]);
+        }
+      }
+    } else {
+      const int r = (int)((s - d) & 15);
+      const uint64_t dend = d + a.rb;
+      V4 carry = v4_zero();
+      // slot c combines source chunks c-1 and c into the destination chunk
+      // D(c) = ws + 16(c-1) + r + (d - s); slots 0..nch cover every destination chunk.
+      for (uint64_t c0 = 0; c0 <= nch; c0 += 32 * U) {
+        V4 cur[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint64_t c = c0 + 32u * u + lane;
+          const uint64_t A = ws + 16ull * c;
+          cur[u] = (ok && c < nch && A + 16 > s) ? ld_chunk<CLIP>(A, a.tbase, tend) : v4_zero();
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint64_t c = c0 + 32u * u + lane;
+          V4 prev = shfl4_up1(cur[u]);
+          if (lane == 0) prev = carry;
+          carry = shfl4(cur[u], 31, 32);
+          const uint64_t D = ws + 16ull * c - 16ull + (uint64_t)r + d - s;
+          st_chunk_clip(D, funnel16(prev, cur[u], r), d, dend);
+        }
+      }
+    }
+    if (!ok && lane == 0) record_bad(a.err, i);
+  }
+}
+
+}  // namespace ut

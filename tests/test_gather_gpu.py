@@ -1,0 +1,196 @@
+"""Parity of the CUDA gather (through the C ABI) with the oracle, element by element (bytes).
+
+Bar: bit-exact (the gather is a pure copy, reading R3). Inputs come from
+``workloads`` only; expected values only from ``oracle``.
+"""
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+
+torch = pytest.importorskip("torch")
+ut = pytest.importorskip("paper_2101_07956_b200")
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+SENT = 0xAB
+
+
+def _gather_check(table, host_addr, rows, rb, idx, out_off=0, plan=None, stream=None):
+    """Run ut_gather into a sentinel-filled buffer at byte offset out_off; compare with oracle."""
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    n = idx.size
+    want, want_bad = oracle.gather(host_addr, rows, rb, idx)
+    if plan is not None:
+        table.set_plan(plan)
+    buf = torch.full((n * rb + out_off + 64,), SENT, dtype=torch.uint8, device="cuda")
+    out = buf[out_off:out_off + n * rb]
+    idx_d = torch.from_numpy(idx).cuda()
+    table.gather(idx_d, out=out, stream=stream)
+    bad = table.error_pos(stream)
+    got = buf.cpu().numpy()
+    assert got[out_off:out_off + n * rb].tobytes() == want.tobytes(), \
+        f"mismatch rb={rb} n={n} off={out_off} plan={table.plan}"
+    assert (got[:out_off] == SENT).all() and (got[out_off + n * rb:] == SENT).all(), "wrote outside out"
+    assert bad == want_bad
+    if plan is not None:
+        table.set_plan("auto")
+
+
+def test_paper_worked_example():
+    g = json.load(open(os.path.join(GOLDEN, "paper_fig5_example.json")))
+    feat = np.array([[100 * i + j for j in range(11)] for i in range(5)], dtype=np.float32)
+    with ut.Table(feat) as t:
+        assert (t.rows, t.row_bytes) == (5, 44)
+        out = t[torch.tensor(g["idx"], device="cuda")]
+        got = out.cpu().numpy().view(np.float32)
+        np.testing.assert_array_equal(got, np.array(g["expected"], dtype=np.float32))
+        _gather_check(t, feat.ctypes.data, 5, 44, g["idx"])
+
+
+@pytest.fixture(scope="module")
+def pinned_pool():
+    """One pinned 48 MiB host region; tables placed inside it are adopted, not re-registered."""
+    pool = torch.empty(48 << 20, dtype=torch.uint8, pin_memory=True)
+    yield pool
+
+
+def test_randomized_instances(pinned_pool):
+    """>= 1000 random (row width, table base, rows, n, out offset, plan) instances."""
+    rng = random.Random(20210119)
+    base_addr = pinned_pool.data_ptr()
+    widths = [1, 2, 3, 4, 5, 7, 8, 12, 16, 17, 24, 31, 32, 33, 48, 64, 68, 100, 127, 128, 129,
+              132, 256, 260, 400, 500, 511, 512, 513, 516, 1024, 1028, 1172, 1372, 2048, 2052,
+              2056, 2064, 2076, 2408, 3200, 4092, 4095, 4096, 5000, 8192, 16384]
+    plans = [None, "realign", "realignx", "vec16", "vec16x", "narrow"]
+    done = 0
+    for it in range(1100):
+        rb = rng.choice(widths) if it % 3 else rng.randint(1, 6000)
+        rows = rng.randint(1, max(1, min(5000, (40 << 20) // rb)))
+        off = rng.randrange(0, 128)
+        nbytes = rows * rb
+        a = pinned_pool[off:off + nbytes].numpy()
+        workloads.fill_table(a, rows, rb, seed=it)
+        n = rng.choice([0, 1, 2, 3, 31, 32, 33, rng.randint(0, 700)])
+        n = min(n, max(1, (4 << 20) // rb))
+        idx = workloads.uniform_idx(n, rows, seed=it + 1)
+        if n and rng.random() < 0.3:
+            idx[rng.randrange(n)] = rows - 1
+        if n and rng.random() < 0.3:
+            idx[rng.randrange(n)] = 0
+        out_off = rng.choice([0, 0, 0, 1, 4, 8, 12, 15])
+        t = ut.Table(base_addr + off, rows, rb)
+        try:
+            assert t.info()["registered"] == 0          # adopted: already pinned
+            plan = rng.choice(plans)
+            if plan is not None:
+                try:
+                    t.set_plan(plan)
+                except ut.UTError:
+                    plan = None
+                t.set_plan("auto")
+            _gather_check(t, base_addr + off, rows, rb, idx, out_off=out_off, plan=plan)
+            done += 1
+        finally:
+            t.close()
+    assert done >= 1000
+
+
+@pytest.mark.parametrize("rb", [1, 3, 4, 8, 13, 16, 68, 100, 400, 512, 2052, 2408, 4096])
+@pytest.mark.parametrize("pad", [0, 1, 7, 9, 15])
+def test_guard_page_no_over_read(rb, pad):
+    """Table ends exactly at a PROT_NONE page; rows placed so the base is misaligned by the
+    residue of -(rows*rb) mod 16. Gathers that include the first and last rows, with every
+    admissible plan, must not fault (an over-read kills the process) and must match."""
+    rows = 37 + pad
+    hb = workloads.HostBuffer(rows * rb, kind="guarded")
+    a = hb.array()
+    workloads.fill_table(a, rows, rb, seed=rb + pad)
+    idx = np.array([rows - 1, 0, rows - 1, rows // 2, 0, rows - 1] * 7, dtype=np.int64)
+    with ut.Table(hb.addr, rows, rb) as t:
+        assert t.info()["registered"] == 1
+        for plan in [None, "realign", "realignx", "vec16", "vec16x", "narrow"]:
+            try:
+                if plan:
+                    t.set_plan(plan)
+            except ut.UTError:
+                continue
+            _gather_check(t, hb.addr, rows, rb, idx, out_off=pad % 16)
+            t.set_plan("auto")
+    torch.cuda.synchronize()
+    del a
+    hb.close()
+
+
+def test_empty_single_last_duplicates_and_out_of_range():
+    rb, rows = 68, 1000
+    hb = workloads.HostBuffer(rows * rb, offset=3)
+    workloads.fill_table(hb.array(), rows, rb, 5)
+    with ut.Table(hb.addr, rows, rb) as t:
+        # n == 0: no launch, out untouched
+        buf = torch.full((16,), SENT, dtype=torch.uint8, device="cuda")
+        t.gather(torch.empty(0, dtype=torch.int64, device="cuda"), out=buf)
+        assert (buf.cpu() == SENT).all()
+        _gather_check(t, hb.addr, rows, rb, [rows - 1])
+        _gather_check(t, hb.addr, rows, rb, [3, 3, 3])
+        _gather_check(t, hb.addr, rows, rb, [5, rows, 7, -1, 9, 1 << 62, -(1 << 62)])
+        _gather_check(t, hb.addr, rows, rb, [-3])
+        assert t.error_pos() == -1                    # cleared by the previous read
+    hb.close()
+    with ut.Table(np.arange(8, dtype=np.uint8), 1, 8) as t:
+        out = t[torch.zeros(5, dtype=torch.int64, device="cuda")]
+        assert (out.cpu().numpy() == np.arange(8)).all()
+
+
+@pytest.mark.parametrize("rb", [4, 400, 2408])
+def test_other_stream_and_consumer_ordering(rb):
+    rows = 20000
+    hb = workloads.HostBuffer(rows * rb)
+    workloads.fill_table(hb.array(), rows, rb, 8)
+    s = torch.cuda.Stream()
+    idx = workloads.uniform_idx(50000, rows, 9)
+    with ut.Table(hb.addr, rows, rb) as t:
+        with torch.cuda.stream(s):
+            idx_d = torch.from_numpy(idx).cuda()
+            out = t.gather(idx_d)
+            ids = out[:, :4].contiguous().view(torch.int32).to(torch.int64)   # consumer on s
+        s.synchronize()
+        np.testing.assert_array_equal(ids.cpu().numpy().reshape(-1), idx & 0xFFFFFFFF)
+        _gather_check(t, hb.addr, rows, rb, idx, stream=s)
+    hb.close()
+
+
+@pytest.mark.parametrize("rb", [4, 68, 400, 2052])
+def test_gather_host_end_to_end(rb):
+    rows = 300_000 if rb < 1000 else 30_000
+    hb = workloads.HostBuffer(rows * rb, offset=rb % 7)
+    workloads.fill_table(hb.array(), rows, rb, 10)
+    idx = workloads.uniform_idx(123_457, rows, 11)
+    idx[5] = rows + 3
+    want, bad = oracle.gather(hb.addr, rows, rb, idx)
+    with ut.Table(hb.addr, rows, rb) as t:
+        idx_h = torch.from_numpy(idx).pin_memory()
+        out = t.gather_host(idx_h)
+        assert out.numpy().tobytes() == want.tobytes()
+        assert t.error_pos() == bad == 5
+    hb.close()
+
+
+def test_register_adopt_and_release():
+    hb = workloads.HostBuffer(1 << 20)
+    t = ut.ut_register(hb.addr, 1024, 1024)
+    assert ut.ut_table_get_info(t)["registered"] == 1
+    t2 = ut.ut_register(hb.addr + 4096, 16, 1024)     # inside pinned pages: adopted
+    assert ut.ut_table_get_info(t2)["registered"] == 0
+    ut.ut_release(t2)                                 # leaves the pages pinned
+    ut.ut_release(t)
+    t = ut.ut_register(hb.addr + 4096, 16, 1024)      # unpinned again: registered afresh
+    info = ut.ut_table_get_info(t)
+    assert info["registered"] == 1 and info["rows"] == 16 and info["dev_addr"] != 0
+    ut.ut_release(t)
+    hb.close()
