@@ -1,0 +1,21 @@
+/*
+ * baselines/cpu_staged.c — the paper's CPU-centric baseline ("Py", Fig. 2a),
+ * reported beside the GPU gather for context (BASELINE.json north_star). Not on the product path.
+ *
+ * The CPU gathers the rows into cache (1) and writes them to a temporary contiguous buffer (2)
+ * with several threads ("the data gathering part of the code is multithreaded"); the
+ * caller then issues one DMA of that buffer to the GPU (3)(4) (cudaMemcpyAsync from pinned
+ * staging, Listing 1 `features[neighbor_id].to("cuda")`).
+ */
+#include <stdint.h>
+#include <string.h>
+#include <omp.h>
+
+void cpu_staged_gather(const uint8_t* table, uint64_t rb, const int64_t* idx, uint64_t n,
+                       uint8_t* staging, int threads)
+{
+    int nt = threads > 0 ? threads : omp_get_max_threads();
+#pragma omp parallel for schedule(static, 256) num_threads(nt)
+    for (int64_t i = 0; i < (int64_t)n; ++i)
+        memcpy(staging + (uint64_t)i * rb, table + (uint64_t)idx[i] * rb, rb);
+}

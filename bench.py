@@ -1,0 +1,498 @@
+#!/usr/bin/env python
+"""bench.py — unified-tensor gather throughput on B200 (PyTorch-Direct, arXiv 2101.07956).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config products|reddit|papers|tiny|sweep:RB]
+                    [--impl ut|reference]
+
+One "step" is one minibatch gather: ``out = table[idx]`` for that step's GraphSAGE-shaped index
+list (Listing 2), every row read by GPU threads straight out of the host-pinned,
+device-mapped table. Each rank (one per GPU, torchrun for N > 1) gathers its own minibatches from
+one shared host table: data parallel by minibatch, no collective on the path ("scaling": "weak").
+
+Printed (rank 0, one JSON line): whole-box useful GB/s (sum of ranks' bytes / max over ranks of
+the summed per-step device time), the kernel's roofline against the host-link ceiling measured in
+the same run (pinned cudaMemcpy H2D, best of 10 x 1 GiB), the end-to-end figure through
+``ut_gather_host`` (host idx in, host rows out), the oracle on the host cores (cpu_baseline), the
+paper's CPU-centric baseline (py_baseline), launch count and clocks.
+
+``--impl reference`` times the oracle (oracle/ut_oracle.c, single-threaded plain C) on the host
+cores on the same workload, as the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+from workloads import graphsage  # noqa: E402
+
+METRIC = "gather GB/s per GPU and per box vs H2D link roofline, 1/2/4/8 B200"
+FLUSH_BYTES = 256 << 20      # > 126 MB L2: written between timed steps
+
+
+# ---- workload ----------------------------------------------------------------------------------
+def workload_spec(config: str) -> dict:
+    """Table shape + index-list recipe of a config (BASELINE.json configs)."""
+    if config in graphsage.CONFIGS:
+        c = graphsage.CONFIGS[config]
+        names = {"reddit": "reddit-shaped", "products": "ogbn-products-shaped",
+                 "papers": "ogbn-papers100M-shaped"}
+        return {"workload": names[config], "kind": "graphsage", "config": config,
+                "rows": c["n_nodes"], "row_bytes": c["row_bytes"], "batch": c["batch"],
+                "fanouts": list(c["fanouts"]), "edges": c["n_edges"]}
+    if config == "tiny":
+        return {"workload": "tiny", "kind": "uniform", "config": config, "rows": 1024,
+                "row_bytes": 68, "n": 512}
+    if config.startswith("sweep:"):
+        rb = int(config.split(":")[1])
+        return {"workload": f"microbenchmark-sweep rb={rb}", "kind": "uniform", "config": config,
+                "rows": (16 << 30) // rb, "row_bytes": rb, "n": 1 << 20}
+    raise ValueError(config)
+
+
+def make_index_lists(spec: dict, rank: int, world: int, count: int, seed: int,
+                     procs: int) -> list[np.ndarray]:
+    """`count` distinct per-rank index lists (generated on the CPU before any timing)."""
+    if spec["kind"] == "uniform":
+        return [workloads.uniform_idx(spec["n"], spec["rows"], seed=seed + 1000003 * (b * world + rank))
+                for b in range(count)]
+    jobs = [(spec["config"], seed, b, rank, world, False) for b in range(count)]
+    if procs > 1 and count > 1:
+        with mp.get_context("fork").Pool(min(procs, count)) as pool:
+            return pool.map(graphsage.minibatch_job, jobs)
+    return [graphsage.minibatch_job(j) for j in jobs]
+
+
+def open_table(spec: dict, rank: int, world: int, seed: int, dist, tag: str):
+    """The shared host feature table: anonymous memory at N=1, a /dev/shm file at N>1 that rank 0
+    creates and fills and every rank maps (one copy on the box)."""
+    rows, rb = spec["rows"], spec["row_bytes"]
+    nbytes = rows * rb
+    threads = os.cpu_count() or 1
+    if world == 1:
+        hb = workloads.HostBuffer(nbytes)
+        workloads.fill_table(hb.addr, rows, rb, seed, threads=threads)
+        return hb
+    name = f"ut_bench_{tag}"
+    if rank == 0:
+        hb = workloads.HostBuffer(nbytes, kind="shm", name=name, create=True)
+        workloads.fill_table(hb.addr, rows, rb, seed, threads=threads)
+    dist.barrier()
+    if rank != 0:
+        hb = workloads.HostBuffer(nbytes, kind="shm", name=name, create=False)
+    dist.barrier()
+    return hb
+
+
+# ---- distributed plumbing ----------------------------------------------------------------------
+class Dist:
+    """Rank facts from the torchrun environment; the process group is created by init()."""
+
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+
+    def init(self, backend: str = "nccl"):
+        if self.world > 1:
+            import torch.distributed as td
+            if backend == "nccl":
+                import torch
+                torch.cuda.set_device(self.local_rank)
+                td.init_process_group(backend="nccl", device_id=torch.device("cuda", self.local_rank))
+            else:
+                td.init_process_group(backend=backend)
+            self.pg = td
+
+    def barrier(self):
+        if self.pg is not None:
+            if self.pg.get_backend() == "nccl":
+                import torch
+                self.pg.barrier(device_ids=[torch.cuda.current_device()])
+            else:
+                self.pg.barrier()
+
+    def allreduce(self, values: list[float], op: str) -> list[float]:
+        if self.pg is None:
+            return list(values)
+        import torch
+        dev = "cuda" if self.pg.get_backend() == "nccl" else "cpu"
+        t = torch.tensor(values, dtype=torch.float64, device=dev)
+        self.pg.all_reduce(t, op={"max": self.pg.ReduceOp.MAX, "sum": self.pg.ReduceOp.SUM}[op])
+        return [float(x) for x in t.cpu()]
+
+    def close(self):
+        if self.pg is not None:
+            self.pg.destroy_process_group()
+
+
+# ---- measurement helpers -----------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms from warm-up to the end of timing."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.lines: list[str] = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for k, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(k)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def h2d_ceiling(torch, nbytes: int = 1 << 30, reps: int = 10) -> float:
+    """Pinned cudaMemcpy H2D ceiling (GB/s): best of `reps` copies of `nbytes`, CUDA events."""
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h.fill_(1)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    best = 0.0
+    for _ in range(reps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        d.copy_(h, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, nbytes / e0.elapsed_time(e1) / 1e6)
+    del h, d
+    return best
+
+
+def cpu_oracle_rate(table_addr: int, spec: dict, lists: list[np.ndarray], budget_s: float):
+    """The oracle as it stands, on this host, over a bounded sample of the same index lists."""
+    import oracle
+    rb = spec["row_bytes"]
+    out = np.empty(max(l.size for l in lists) * rb, dtype=np.uint8)
+    done_bytes, done_lists, t0 = 0, 0, time.perf_counter()
+    while True:
+        l = lists[done_lists % len(lists)]
+        oracle.gather_into(table_addr, spec["rows"], rb, l, out)
+        done_bytes += l.size * rb
+        done_lists += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or done_lists >= 4 * len(lists):
+            break
+    return done_bytes / el / 1e9, done_lists, el
+
+
+# ---- the arms ------------------------------------------------------------------------------------
+def run_reference(args, spec, dist):
+    """Reference arm: the oracle on the host cores, K timed steps of one minibatch each.
+    Under torchrun only rank 0 runs it; the other ranks exit without work."""
+    if dist.rank != 0:
+        return
+    import oracle
+    seed = args.seed
+    lists = make_index_lists(spec, 0, 1, args.warmup + args.steps, seed, os.cpu_count() or 1)
+    hb = open_table(spec, 0, 1, seed, None, "ref")
+    rb = spec["row_bytes"]
+    out = np.empty(max(l.size for l in lists) * rb, dtype=np.uint8)
+    for s in range(args.warmup):
+        oracle.gather_into(hb.addr, spec["rows"], rb, lists[s], out)
+    t0 = time.perf_counter()
+    nbytes = 0
+    for s in range(args.steps):
+        l = lists[args.warmup + s]
+        oracle.gather_into(hb.addr, spec["rows"], rb, l, out)
+        nbytes += l.size * rb
+    el = time.perf_counter() - t0
+    value = nbytes / el / 1e9
+    line = {"metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "impl": "reference",
+            "config": config_block(spec, lists[args.warmup:], args.gpus),
+            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1,
+                             "kind": "oracle",
+                             "sample": f"{args.steps} full minibatches of the workload, single-threaded plain C"},
+            "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    hb.close()
+
+
+def config_block(spec: dict, lists, world: int) -> dict:
+    rows_per_step = float(np.mean([l.size for l in lists])) if lists else 0.0
+    c = {"workload": spec["workload"], "table_rows": spec["rows"], "row_bytes": spec["row_bytes"],
+         "table_gb": round(spec["rows"] * spec["row_bytes"] / 1e9, 3),
+         "rows_per_step_per_gpu": round(rows_per_step, 1),
+         "mb_per_step_per_gpu": round(rows_per_step * spec["row_bytes"] / 1e6, 2),
+         "parallelism": f"dp{world} (independent minibatches per GPU, one shared host table)",
+         "l2": "flushed (256 MiB write) between timed steps, outside the per-step events"}
+    if spec["kind"] == "graphsage":
+        c.update({"batch": spec["batch"], "fanouts": spec["fanouts"], "graph_edges": spec["edges"]})
+    else:
+        c["n_per_step"] = spec["n"]
+    return c
+
+
+def run_ut(args, spec, dist):
+    import torch
+
+    rank, world = dist.rank, dist.world
+    seed = args.seed
+    count = min(args.warmup + args.steps, args.max_lists)
+    procs = max(1, (os.cpu_count() or 1) // world)
+    lists = make_index_lists(spec, rank, world, count, seed + 17, procs)   # before CUDA init
+
+    torch.cuda.set_device(dist.local_rank)
+    dist.init(args.backend)
+    import paper_2101_07956_b200 as ut
+
+    tag = f"{spec['config'].replace(':', '_')}_{os.environ.get('MASTER_PORT', '0')}"
+    hb = open_table(spec, rank, world, seed, dist, tag)
+    t_reg = time.perf_counter()
+    table = ut.Table(hb.addr, spec["rows"], spec["row_bytes"])
+    reg_s = time.perf_counter() - t_reg
+    if args.plan:
+        for p in args.plan.split(","):
+            table.set_plan(p)
+    rb = spec["row_bytes"]
+    stream = torch.cuda.current_stream()
+    idx_dev = [torch.from_numpy(l).to("cuda") for l in lists]
+    max_n = max(l.size for l in lists)
+    out = torch.empty(max_n * rb, dtype=torch.uint8, device="cuda")
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+
+    # roofline denominator, measured now, on every rank at once (concurrent ceiling at N > 1)
+    dist.barrier()
+    link = h2d_ceiling(torch)
+    link_sum = dist.allreduce([link], "sum")[0]
+
+    # parity (outside timing): the first minibatch against the oracle, byte for byte
+    parity = None
+    if args.check:
+        import oracle
+        l = lists[0]
+        want, bad = oracle.gather(hb.addr, spec["rows"], rb, l)
+        table.gather(idx_dev[0], out=out[: l.size * rb])
+        got = out[: l.size * rb].cpu().numpy()
+        parity = bool(got.tobytes() == want.tobytes()) and table.error_pos() == bad
+        if not parity:
+            raise SystemExit(f"rank {rank}: parity failure on minibatch 0")
+
+    clocks = ClockSampler(dist.local_rank)
+    clocks.start()
+    # warm-up
+    for s in range(args.warmup):
+        l = idx_dev[s % count]
+        table.gather(l, out=out[: l.numel() * rb])
+    torch.cuda.synchronize()
+
+    table.set_plan("timing=on")
+    table.stats(reset=True)
+    evs = []
+    nbytes = 0
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        l = idx_dev[(args.warmup + s) % count]
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        table.gather(l, out=out[: l.numel() * rb], stream=stream)
+        e1.record(stream)
+        evs.append((e0, e1))
+        nbytes += l.numel() * rb
+    torch.cuda.synchronize()
+    dist.barrier()
+    wall = time.perf_counter() - t0
+    clk = clocks.stop()
+    st = table.stats(reset=True)
+    table.set_plan("timing=off")
+    dev_ms = sum(a.elapsed_time(b) for a, b in evs)
+
+    red = dist.allreduce([dev_ms, wall], "max")
+    tot = dist.allreduce([float(nbytes), float(st["kernel_launches"])], "sum")
+    max_dev_ms, max_wall = red
+    box_bytes, launches = tot
+    value = box_bytes / (max_dev_ms / 1e3) / 1e9
+    per_gpu = nbytes / (dev_ms / 1e3) / 1e9
+    kern_ms = st["gather_kernel_ms"] / max(1, st["timed_launches"])
+    kern_bytes = nbytes / max(1, st["timed_launches"])
+    achieved = kern_bytes / (kern_ms / 1e3) / 1e9 if kern_ms > 0 else 0.0
+
+    # end to end: host idx in (pinned), host rows out (pinned), through ut_gather_host
+    e2e = None
+    if not args.no_e2e:
+        idx_host = [torch.from_numpy(x).pin_memory() for x in lists]
+        out_host = torch.empty(max_n * rb, dtype=torch.uint8, pin_memory=True)
+        for s in range(min(2, count)):
+            table.gather_host(idx_host[s], out_host=out_host)
+        e_sec, e_bytes, h2d, d2h = 0.0, 0, 0, 0
+        for s in range(args.steps):
+            ih = idx_host[(args.warmup + s) % count]
+            flush.zero_()
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            table.gather_host(ih, out_host=out_host)
+            e_sec += time.perf_counter() - t1
+            e_bytes += ih.numel() * rb
+            h2d += ih.numel() * 8
+            d2h += ih.numel() * rb
+        mx = dist.allreduce([e_sec], "max")[0]
+        e_tot = dist.allreduce([float(e_bytes)], "sum")[0]
+        e2e = {"value": round(e_tot / mx / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps),
+               "path": "ut_gather_host: idx H2D + gather + rows D2H, chunked on two streams"}
+        del out_host, idx_host
+
+    # context baselines on rank 0 at N=1: the oracle and the paper's CPU-centric path
+    cpu_base, py_base = None, None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, nl, el = cpu_oracle_rate(hb.addr, spec, lists, args.cpu_budget)
+        cpu_base = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                    "sample": f"{nl} minibatches of the workload in {el:.1f} s, single-threaded plain C"}
+        py_base = cpu_staged_baseline(torch, hb.addr, spec, lists, args)
+
+    if rank == 0:
+        n_launch = int(launches)
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(max_dev_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (self-identifying fp32-row table, GraphSAGE-shaped index lists)",
+            "config": config_block(spec, lists[args.warmup:] or lists, world),
+            "per_gpu_gbs": round(per_gpu, 3),
+            "h2d_memcpy_gbs": round(link, 3),
+            "h2d_memcpy_concurrent_gbs": round(link_sum, 3),
+            "frac_of_link": round(per_gpu / link, 4),
+            "plan": table.plan,
+            "roofline": {"bound": "pcie_h2d", "achieved": round(achieved, 3),
+                         "peak": round(link, 3), "unit": "GB/s",
+                         "frac": round(achieved / link, 4), "traffic": None,
+                         "kernel": f"gather {table.plan} (device time of the gather kernel alone, CUDA events on its stream)",
+                         "peak_source": "pinned cudaMemcpy H2D measured in this run (best of 10 x 1 GiB)"},
+            "cpu_baseline": cpu_base, "py_baseline": py_base, "e2e": e2e,
+            "gpu_launches": n_launch, "clocks": clk,
+            "parity_checked": parity, "register_s": round(reg_s, 3),
+            "wall_ms_per_step": round(max_wall / args.steps * 1e3, 3),
+        }
+        print(json.dumps(line), flush=True)
+    table.close()
+    dist.barrier()
+    if world > 1 and rank == 0:
+        hb.close(unlink=True)
+    else:
+        hb.close()
+
+
+def cpu_staged_baseline(torch, table_addr, spec, lists, args):
+    """The paper's "Py" path (Fig. 2a): all host cores gather into pinned staging, one H2D DMA."""
+    import baselines
+    rb = spec["row_bytes"]
+    max_n = max(l.size for l in lists)
+    staging = torch.empty(max_n * rb, dtype=torch.uint8, pin_memory=True)
+    dev = torch.empty(max_n * rb, dtype=torch.uint8, device="cuda")
+    threads = os.cpu_count() or 1
+    steps = min(len(lists), max(3, args.steps // 2))
+    sec, nbytes = 0.0, 0
+    for s in range(steps + 1):
+        l = lists[s % len(lists)]
+        b = l.size * rb
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        baselines.cpu_staged_gather(table_addr, rb, l.ctypes.data, l.size, staging.data_ptr(), threads)
+        dev[:b].copy_(staging[:b], non_blocking=True)
+        torch.cuda.synchronize()
+        if s > 0:
+            sec += time.perf_counter() - t0
+            nbytes += b
+    return {"value": round(nbytes / sec / 1e9, 3), "unit": "GB/s", "threads": threads,
+            "kind": "CPU gather into pinned staging + cudaMemcpyAsync H2D (PAPER.md:221-225)",
+            "steps": steps}
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="products")
+    ap.add_argument("--impl", default="ut", choices=["ut", "reference"])
+    ap.add_argument("--seed", type=int, default=2101)
+    ap.add_argument("--plan", default="", help="comma list passed to ut_set_plan (A/B runs)")
+    ap.add_argument("--max-lists", type=int, default=64, help="distinct minibatches per rank")
+    ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of oracle timing")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-check", dest="check", action="store_false")
+    ap.add_argument("--backend", default="nccl", help="process-group backend at N > 1")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    spec = workload_spec(args.config)
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            run_reference(args, spec, dist)
+        else:
+            run_ut(args, spec, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

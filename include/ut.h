@@ -147,12 +147,35 @@ UT_API const char* ut_plan_name(const ut_table* t);
 UT_API const char* ut_plan_probe(uint64_t base, uint64_t rows, uint64_t row_bytes, uint64_t out);
 
 /*
- * ut_set_plan — force a variant by name for A/B measurement ("auto" restores the automatic
- * choice). Any variant accepted here is correct for any alignment it admits; a variant whose
- * preconditions the table violates returns UT_EINVAL and leaves the plan unchanged.
- * The environment variable UT_PLAN, read at ut_register, has the same effect.
+ * ut_set_plan — force a kernel variant by kind for A/B measurement: "narrow", "vec16",
+ * "vec16x", "realign", "realignx", or "auto" (the default choice). A kind whose preconditions
+ * the table violates returns UT_EINVAL and leaves the plan unchanged; every admissible kind is
+ * correct for any output alignment (ut_gather falls back to "auto" for an output it cannot take).
+ * "timing=on|off" brackets each gather-kernel launch with CUDA events (see ut_get_stats).
+ * "reorder=on|off|auto" controls the translation-locality stage instead:
+ * work items are visited grouped by the 2-MiB table region their row lies in, the output order
+ * is unchanged; "auto" enables it for tables > 1 GiB and gathers of >= 4 MiB.
+ * The environment variables UT_PLAN and UT_REORDER, read at ut_register, do the same.
  */
 UT_API int ut_set_plan(ut_table* t, const char* name);
+
+/* Per-device counters of one table (for reports and the bench's launch count). */
+typedef struct ut_stats {
+  uint64_t gathers;          /* gather-kernel launches (one per ut_gather, per chunk of ut_gather_host) */
+  uint64_t kernel_launches;  /* every kernel this library launched (gather + reorder stage)           */
+  uint64_t rows;             /* rows gathered                                                        */
+  uint64_t bytes;            /* rows * row_bytes                                                     */
+  uint64_t timed_launches;   /* gather-kernel launches bracketed by events ("timing=on")            */
+  double gather_kernel_ms;   /* their summed device time (CUDA events on the launch stream)          */
+} ut_stats;
+
+/*
+ * ut_get_stats — counters of table t on the current device since registration or the last
+ * reset. With "timing=on" (ut_set_plan) every gather-kernel launch is bracketed by CUDA events
+ * on its stream; this call waits for the pending events and adds their durations. reset != 0
+ * zeroes the counters afterwards. Returns UT_OK, UT_EINVAL or UT_ECUDA.
+ */
+UT_API int ut_get_stats(const ut_table* t, ut_stats* stats, int reset);
 
 /* Table facts recorded at registration (for tests and reports). */
 typedef struct ut_table_info {

@@ -9,7 +9,7 @@ Low level (same names and arguments as the C ABI, raw addresses and ints):
     ut_register(host_addr, rows, row_bytes) -> handle
     ut_gather(handle, idx_dev_addr, n, out_dev_addr, stream_handle)
     ut_gather_host(handle, idx_host_addr, n, out_host_addr, stream_handle)
-    ut_release(handle), ut_error_pos(handle, stream_handle) -> int,
+    ut_release(handle), ut_error_pos(handle, stream_handle) -> int, ut_get_stats(handle),
     ut_plan_name(handle), ut_set_plan(handle, name), ut_plan_probe(base, rows, rb, out),
     ut_table_get_info(handle) -> dict
 
@@ -27,7 +27,8 @@ UT_OK, UT_EINVAL, UT_ENOMEM, UT_ECUDA, UT_ERANGE, UT_ENOTSUP = 0, -1, -2, -3, -4
 
 # Every symbol include/ut.h declares (tests check the library exports exactly these).
 ABI = ("ut_register", "ut_gather", "ut_gather_host", "ut_release", "ut_error_pos",
-       "ut_last_error", "ut_plan_name", "ut_plan_probe", "ut_set_plan", "ut_table_get_info")
+       "ut_last_error", "ut_plan_name", "ut_plan_probe", "ut_set_plan", "ut_table_get_info",
+       "ut_get_stats")
 
 
 class UTError(RuntimeError):
@@ -41,6 +42,12 @@ class _Info(ctypes.Structure):
                 ("host_addr", ctypes.c_uint64), ("dev_addr", ctypes.c_uint64),
                 ("registered", ctypes.c_int), ("read_only", ctypes.c_int),
                 ("base_mod128", ctypes.c_int), ("device", ctypes.c_int)]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("gathers", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
+                ("rows", ctypes.c_uint64), ("bytes", ctypes.c_uint64),
+                ("timed_launches", ctypes.c_uint64), ("gather_kernel_ms", ctypes.c_double)]
 
 
 def _load():
@@ -67,6 +74,8 @@ def _load():
     L.ut_set_plan.argtypes = [vp, ctypes.c_char_p]
     L.ut_table_get_info.restype = ctypes.c_int
     L.ut_table_get_info.argtypes = [vp, ctypes.POINTER(_Info)]
+    L.ut_get_stats.restype = ctypes.c_int
+    L.ut_get_stats.argtypes = [vp, ctypes.POINTER(_Stats), ctypes.c_int]
     return L
 
 
@@ -134,6 +143,12 @@ def ut_table_get_info(t: int) -> dict:
     return {k: getattr(info, k) for k, _ in _Info._fields_}
 
 
+def ut_get_stats(t: int, reset: bool = False) -> dict:
+    st = _Stats()
+    _check(_lib.ut_get_stats(t, ctypes.byref(st), 1 if reset else 0))
+    return {k: getattr(st, k) for k, _ in _Stats._fields_}
+
+
 # ---- convenience ----------------------------------------------------------------------------
 def _stream_handle(stream) -> int:
     import torch
@@ -181,6 +196,9 @@ class Table:
 
     def info(self) -> dict:
         return ut_table_get_info(self.handle)
+
+    def stats(self, reset: bool = False) -> dict:
+        return ut_get_stats(self.handle, reset)
 
     def gather(self, idx, out=None, stream=None):
         """out[i] = row idx[i] (uint8 [n, row_bytes] CUDA tensor); idx: CUDA int64 tensor."""

@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <vector>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -135,6 +137,13 @@ struct DevState {
   uint64_t dev_base = 0;               // device address of the table on this device
   unsigned long long* err = nullptr;   // first out-of-range position, ~0 = none
   int sms = 0;
+  cudaMemPool_t pool = nullptr;         // stream-ordered scratch for the reorder stage
+  // counters (ut_get_stats)
+  std::atomic<uint64_t> gathers{0}, launches{0}, rows{0}, bytes{0};
+  std::mutex tmu;                       // timing events
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending, spare;
+  uint64_t timed = 0;
+  double timed_ms = 0.0;
   // ut_gather_host scratch
   static constexpr int kBuf = 3;
   int64_t* idx_buf[kBuf] = {};
@@ -154,6 +163,8 @@ struct ut_table {
   uint64_t reg_len = 0;
   int registered = 0, read_only = 0, device = 0;
   PlanKind forced = P_AUTO;
+  int reorder = -1;                     // -1 auto, 0 off, 1 on (ut_set_plan "reorder=...")
+  bool timing = false;                  // ut_set_plan "timing=on"
   std::mutex mu;
   DevState dev[kMaxDev];
 };
@@ -184,6 +195,16 @@ int dev_state(const ut_table* ct, DevState** out) {
     if (e != cudaSuccess) return cuda_err(e, "cudaMemset(error word)");
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    e = cudaMemPoolCreate(&pool, &props);
+    if (e != cudaSuccess) return cuda_err(e, "cudaMemPoolCreate");
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    s->pool = pool;
     s->dev_base = (uint64_t)dp + (uint64_t)(t->host - t->reg_base);
     s->err = err;
     s->sms = sms > 0 ? sms : 148;
@@ -213,53 +234,54 @@ cudaError_t launch(K kernel, int grid, cudaStream_t st, const ut::GatherArgs& a)
   return cudaGetLastError();
 }
 
-template <int G>
+template <int G, bool PERM>
 cudaError_t launch_single(const Plan& p, int sms, cudaStream_t st, const ut::GatherArgs& a) {
   constexpr uint64_t rpt = (32 / G) * kU;
   const uint64_t tiles = (a.n + rpt - 1) / rpt;
   if (p.kind == P_VEC16) {
-    auto k = ut::k_single<G, kU, true, false>;
+    auto k = ut::k_single<G, kU, true, false, PERM>;
     return launch(k, grid_for(k, sms, tiles), st, a);
   }
   if (p.clip) {
-    auto k = ut::k_single<G, kU, false, true>;
+    auto k = ut::k_single<G, kU, false, true, PERM>;
     return launch(k, grid_for(k, sms, tiles), st, a);
   }
-  auto k = ut::k_single<G, kU, false, false>;
+  auto k = ut::k_single<G, kU, false, false, PERM>;
   return launch(k, grid_for(k, sms, tiles), st, a);
 }
 
+template <bool PERM>
 cudaError_t launch_plan(const Plan& p, int sms, cudaStream_t st, const ut::GatherArgs& a) {
   switch (p.kind) {
     case P_NARROW: {
       const uint64_t warps = (a.n + 32 * kUn - 1) / (32 * kUn);
       switch (p.g) {
-        case 1: { auto k = ut::k_narrow<uint8_t, kUn>; return launch(k, grid_for(k, sms, warps), st, a); }
-        case 2: { auto k = ut::k_narrow<uint16_t, kUn>; return launch(k, grid_for(k, sms, warps), st, a); }
-        case 4: { auto k = ut::k_narrow<uint32_t, kUn>; return launch(k, grid_for(k, sms, warps), st, a); }
-        default: { auto k = ut::k_narrow<uint64_t, kUn>; return launch(k, grid_for(k, sms, warps), st, a); }
+        case 1: { auto k = ut::k_narrow<uint8_t, kUn, PERM>; return launch(k, grid_for(k, sms, warps), st, a); }
+        case 2: { auto k = ut::k_narrow<uint16_t, kUn, PERM>; return launch(k, grid_for(k, sms, warps), st, a); }
+        case 4: { auto k = ut::k_narrow<uint32_t, kUn, PERM>; return launch(k, grid_for(k, sms, warps), st, a); }
+        default: { auto k = ut::k_narrow<uint64_t, kUn, PERM>; return launch(k, grid_for(k, sms, warps), st, a); }
       }
     }
     case P_VEC16:
     case P_REALIGN:
       switch (p.g) {
-        case 1: return launch_single<1>(p, sms, st, a);
-        case 2: return launch_single<2>(p, sms, st, a);
-        case 4: return launch_single<4>(p, sms, st, a);
-        case 8: return launch_single<8>(p, sms, st, a);
-        case 16: return launch_single<16>(p, sms, st, a);
-        default: return launch_single<32>(p, sms, st, a);
+        case 1: return launch_single<1, PERM>(p, sms, st, a);
+        case 2: return launch_single<2, PERM>(p, sms, st, a);
+        case 4: return launch_single<4, PERM>(p, sms, st, a);
+        case 8: return launch_single<8, PERM>(p, sms, st, a);
+        case 16: return launch_single<16, PERM>(p, sms, st, a);
+        default: return launch_single<32, PERM>(p, sms, st, a);
       }
     case P_VEC16X: {
-      auto k = ut::k_multi<kUx, true, false>;
+      auto k = ut::k_multi<kUx, true, false, PERM>;
       return launch(k, grid_for(k, sms, a.n), st, a);
     }
     case P_REALIGNX: {
       if (p.clip) {
-        auto k = ut::k_multi<kUx, false, true>;
+        auto k = ut::k_multi<kUx, false, true, PERM>;
         return launch(k, grid_for(k, sms, a.n), st, a);
       }
-      auto k = ut::k_multi<kUx, false, false>;
+      auto k = ut::k_multi<kUx, false, false, PERM>;
       return launch(k, grid_for(k, sms, a.n), st, a);
     }
     default:
@@ -267,16 +289,102 @@ cudaError_t launch_plan(const Plan& p, int sms, cudaStream_t st, const ut::Gathe
   }
 }
 
+// Translation reorder policy. The GPU's translation of the mapped table
+// covers about 1 GiB at full speed (measured: random rows over a 16-GiB table run at 56 vs
+// 100 Mrows/s, 2-MiB-bucketed rows at 100); beyond that, visiting the rows grouped by 2-MiB
+// region restores link-bound speed. Worth its ~4 small launches only for large gathers.
+bool want_reorder(const ut_table* t, uint64_t n);
+
+template <bool PERM>
+cudaError_t timed_launch(const ut_table* t, DevState* s, const Plan& p, cudaStream_t st,
+                         const ut::GatherArgs& a);
+
+int bucket_shift(uint64_t table_bytes) {
+  int shift = 21;                                   // 2-MiB regions
+  while ((table_bytes >> shift) >= 65536) ++shift;  // at most 64K buckets
+  return shift;
+}
 int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n, void* out_dev,
               cudaStream_t st) {
   Plan p;
   if (!choose_plan((uint64_t)t->host, t->rows, t->rb, (uint64_t)out_dev, t->forced, &p) &&
       !choose_plan((uint64_t)t->host, t->rows, t->rb, (uint64_t)out_dev, P_AUTO, &p))
     return set_err(UT_EINVAL, "no admissible plan");
-  ut::GatherArgs a{s->dev_base, t->rows, t->rb, idx_dev, n, (uint64_t)out_dev, s->err};
-  cudaError_t e = launch_plan(p, s->sms, st, a);
-  if (e != cudaSuccess) return cuda_err(e, plan_name(p));
+  ut::GatherArgs a{s->dev_base, t->rows, t->rb, idx_dev, n, (uint64_t)out_dev, s->err, nullptr};
+  cudaError_t e;
+  s->rows += n;
+  s->bytes += n * t->rb;
+  if (!want_reorder(t, n)) {
+    e = timed_launch<false>(t, s, p, st, a);
+    if (e != cudaSuccess) return cuda_err(e, plan_name(p));
+    return UT_OK;
+  }
+  // counting sort of the work items by 2-MiB table region (stream-ordered scratch from the
+  // library's pool); n < 2^32 per launch, larger gathers are split.
+  const int shift = bucket_shift(t->bytes);
+  const uint32_t nb = (uint32_t)(((t->bytes - 1) >> shift) + 1);
+  const uint64_t chunk = 1ull << 31;
+  for (uint64_t off = 0; off < n; off += chunk) {
+    const uint64_t cnt_n = std::min(chunk, n - off);
+    uint32_t* scratch = nullptr;
+    const size_t bytes = ((size_t)nb + cnt_n) * sizeof(uint32_t);
+    if ((e = cudaMallocFromPoolAsync((void**)&scratch, bytes, s->pool, st)) != cudaSuccess)
+      return cuda_err(e, "cudaMallocFromPoolAsync(reorder scratch)");
+    uint32_t* cnt = scratch;
+    uint32_t* perm = scratch + nb;
+    ut::GatherArgs c = a;
+    c.idx = idx_dev + off;
+    c.n = cnt_n;
+    c.out = (uint64_t)out_dev + off * t->rb;
+    c.perm = perm;
+    const int grid = (int)std::min<uint64_t>((uint64_t)s->sms * 8, (cnt_n + 255) / 256);
+    if ((e = cudaMemsetAsync(cnt, 0, nb * sizeof(uint32_t), st)) != cudaSuccess)
+      return cuda_err(e, "cudaMemsetAsync(buckets)");
+    ut::k_bucket_count<<<grid, 256, 0, st>>>(c, shift, cnt);
+    ut::k_bucket_scan<<<1, 1024, 0, st>>>(cnt, nb);
+    ut::k_bucket_scatter<<<grid, 256, 0, st>>>(c, shift, cnt, perm);
+    s->launches += 3;
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = timed_launch<true>(t, s, p, st, c);
+    cudaError_t e2 = cudaFreeAsync(scratch, st);
+    if (e != cudaSuccess) return cuda_err(e, plan_name(p));
+    if (e2 != cudaSuccess) return cuda_err(e2, "cudaFreeAsync(reorder scratch)");
+  }
   return UT_OK;
+}
+
+template <bool PERM>
+cudaError_t timed_launch(const ut_table* t, DevState* s, const Plan& p, cudaStream_t st,
+                         const ut::GatherArgs& a) {
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (t->timing) {
+    std::lock_guard<std::mutex> lk(s->tmu);
+    if (!s->spare.empty()) {
+      ev = s->spare.back();
+      s->spare.pop_back();
+    } else {
+      cudaEventCreate(&ev.first);
+      cudaEventCreate(&ev.second);
+    }
+    cudaEventRecord(ev.first, st);
+  }
+  cudaError_t e = launch_plan<PERM>(p, s->sms, st, a);
+  if (e == cudaSuccess) {
+    s->gathers += 1;
+    s->launches += 1;
+  }
+  if (t->timing) {
+    cudaEventRecord(ev.second, st);
+    std::lock_guard<std::mutex> lk(s->tmu);
+    s->pending.push_back(ev);
+  }
+  return e;
+}
+
+bool want_reorder(const ut_table* t, uint64_t n) {
+  if (t->reorder == 0) return false;
+  if (t->reorder == 1) return true;
+  return t->bytes > (1ull << 30) && n * t->rb >= (4ull << 20) && n >= 4096;
 }
 
 }  // namespace
@@ -350,6 +458,8 @@ ut_table* ut_register(const void* host_ptr, uint64_t rows, uint64_t row_bytes) {
     Plan p;
     if (ok && (k == P_AUTO || choose_plan((uint64_t)t->host, rows, row_bytes, 0, k, &p))) t->forced = k;
   }
+  const char* renv = getenv("UT_REORDER");
+  if (renv && *renv) t->reorder = !strcmp(renv, "on") ? 1 : !strcmp(renv, "off") ? 0 : -1;
   DevState* s;
   if (dev_state(t, &s) != UT_OK) {
     char msg[512];
@@ -454,6 +564,15 @@ int ut_release(ut_table* t) {
       if (s.drained[b]) cudaEventDestroy(s.drained[b]);
     }
     if (s.copy_stream) cudaStreamDestroy(s.copy_stream);
+    for (auto* v : {&s.pending, &s.spare})
+      for (auto& ev : *v) {
+        cudaEventDestroy(ev.first);
+        cudaEventDestroy(ev.second);
+      }
+    if (s.pool) {
+      cudaDeviceSynchronize();
+      cudaMemPoolDestroy(s.pool);
+    }
   }
   cudaSetDevice(cur);
   if (t->registered) {
@@ -511,6 +630,18 @@ const char* ut_plan_probe(uint64_t base, uint64_t rows, uint64_t row_bytes, uint
 
 int ut_set_plan(ut_table* t, const char* name) {
   if (!t || !name) return set_err(UT_EINVAL, "NULL argument");
+  if (!strcmp(name, "timing=on") || !strcmp(name, "timing=off")) {
+    t->timing = name[8] == 'n';
+    return UT_OK;
+  }
+  if (!strncmp(name, "reorder=", 8)) {
+    const char* v = name + 8;
+    if (!strcmp(v, "auto")) t->reorder = -1;
+    else if (!strcmp(v, "on")) t->reorder = 1;
+    else if (!strcmp(v, "off")) t->reorder = 0;
+    else return set_err(UT_EINVAL, "reorder must be auto|on|off, got '%s'", v);
+    return UT_OK;
+  }
   bool ok;
   PlanKind k = parse_plan(name, &ok);
   if (!ok) return set_err(UT_EINVAL, "unknown plan '%s'", name);
@@ -518,6 +649,39 @@ int ut_set_plan(ut_table* t, const char* name) {
   if (k != P_AUTO && !choose_plan((uint64_t)t->host, t->rows, t->rb, 0, k, &p))
     return set_err(UT_EINVAL, "plan '%s' not admissible for this table", name);
   t->forced = k;
+  return UT_OK;
+}
+
+int ut_get_stats(const ut_table* t, ut_stats* st, int reset) {
+  if (!t || !st) return set_err(UT_EINVAL, "NULL argument");
+  DevState* s;
+  int rc = dev_state(t, &s);
+  if (rc != UT_OK) return rc;
+  std::lock_guard<std::mutex> lk(s->tmu);
+  for (auto& ev : s->pending) {
+    cudaError_t e = cudaEventSynchronize(ev.second);
+    if (e != cudaSuccess) return cuda_err(e, "cudaEventSynchronize");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev.first, ev.second);
+    s->timed_ms += ms;
+    s->timed += 1;
+    s->spare.push_back(ev);
+  }
+  s->pending.clear();
+  st->gathers = s->gathers;
+  st->kernel_launches = s->launches;
+  st->rows = s->rows;
+  st->bytes = s->bytes;
+  st->timed_launches = s->timed;
+  st->gather_kernel_ms = s->timed_ms;
+  if (reset) {
+    s->gathers = 0;
+    s->launches = 0;
+    s->rows = 0;
+    s->bytes = 0;
+    s->timed = 0;
+    s->timed_ms = 0.0;
+  }
   return UT_OK;
 }
 

@@ -141,7 +141,16 @@ struct GatherArgs {
   uint64_t n;
   uint64_t out;     // device address of out byte 0
   unsigned long long* err;
+  const uint32_t* perm;   // optional visiting order (work item j handles output row perm[j])
 };
+
+// Output row handled by work item j: j itself, or perm[j] when the rows are visited in the
+// translation-locality order built by k_bucket_* (DESIGN.md §Reorder).
+template <bool PERM>
+__device__ __forceinline__ uint64_t row_of(const GatherArgs& a, uint64_t j, bool inb) {
+  if (!PERM) return j;
+  return inb ? (uint64_t)__ldg(a.perm + j) : 0ull;
+}
 
 __device__ __forceinline__ void record_bad(unsigned long long* err, uint64_t i) {
   atomicMin(err, (unsigned long long)i);
@@ -149,24 +158,26 @@ __device__ __forceinline__ void record_bad(unsigned long long* err, uint64_t i) 
 
 // ---------------------------------------------------------------------------------------------
 // narrow<T>: one thread per row, U rows per thread in flight.
-template <typename T, int U>
+template <typename T, int U, bool PERM>
 __global__ void __launch_bounds__(256) k_narrow(GatherArgs a) {
   const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (uint64_t base = 0; base < a.n; base += nthreads * U) {
     T v[U];
     bool inb[U], ok[U];
+    uint64_t ii[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      uint64_t i = base + (uint64_t)u * nthreads + t0;
-      inb[u] = i < a.n;
+      const uint64_t j = base + (uint64_t)u * nthreads + t0;
+      inb[u] = j < a.n;
+      const uint64_t i = ii[u] = row_of<PERM>(a, j, inb[u]);
       int64_t r = inb[u] ? __ldg(a.idx + i) : 0;
       ok[u] = inb[u] && (uint64_t)r < a.rows;
       v[u] = ok[u] ? *reinterpret_cast<const T*>(a.tbase + (uint64_t)r * sizeof(T)) : T(0);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      uint64_t i = base + (uint64_t)u * nthreads + t0;
+      const uint64_t i = ii[u];
       if (inb[u]) {
         *reinterpret_cast<T*>(a.out + i * sizeof(T)) = v[u];
         if (!ok[u]) record_bad(a.err, i);
@@ -178,7 +189,7 @@ __global__ void __launch_bounds__(256) k_narrow(GatherArgs a) {
 // ---------------------------------------------------------------------------------------------
 // Single-pass kernels: G lanes per row, 32/G rows per warp step, U steps in flight per warp tile.
 // ALIGNED: base, rb, out 16-B aligned (vec16<G>); else realign<G>.
-template <int G, int U, bool ALIGNED, bool CLIP>
+template <int G, int U, bool ALIGNED, bool CLIP, bool PERM>
 __global__ void __launch_bounds__(256) k_single(GatherArgs a) {
   constexpr int RPS = 32 / G;          // rows per warp step
   constexpr int RPT = RPS * U;         // rows per warp tile
@@ -192,12 +203,13 @@ __global__ void __launch_bounds__(256) k_single(GatherArgs a) {
 
   for (uint64_t tile = warp; tile < ntiles; tile += nwarps) {
     V4 cur[U];
-    uint64_t s[U];
+    uint64_t s[U], ii[U];
     bool inb[U], ok[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const uint64_t i = tile * RPT + (uint64_t)u * RPS + grp;
-      inb[u] = i < a.n;
+      const uint64_t j = tile * RPT + (uint64_t)u * RPS + grp;
+      inb[u] = j < a.n;
+      const uint64_t i = ii[u] = row_of<PERM>(a, j, inb[u]);
       const int64_t r = inb[u] ? __ldg(a.idx + i) : 0;
       ok[u] = inb[u] && (uint64_t)r < a.rows;
       s[u] = a.tbase + (ok[u] ? (uint64_t)r : 0ull) * a.rb;
@@ -212,7 +224,7 @@ __global__ void __launch_bounds__(256) k_single(GatherArgs a) {
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const uint64_t i = tile * RPT + (uint64_t)u * RPS + grp;
+      const uint64_t i = ii[u];
       const uint64_t d = a.out + i * a.rb;
       if (ALIGNED) {
         if (inb[u] && (uint64_t)q * 16 < a.rb) st16(d + 16ull * q, cur[u]);
@@ -240,14 +252,15 @@ __global__ void __launch_bounds__(256) k_single(GatherArgs a) {
 // ---------------------------------------------------------------------------------------------
 // Multi-pass kernels: one warp per row, the row's source window starts on a 128-B line and is
 // walked 32*U chunks at a time (U LDG.128 per lane in flight).
-template <int U, bool ALIGNED, bool CLIP>
+template <int U, bool ALIGNED, bool CLIP, bool PERM>
 __global__ void __launch_bounds__(256) k_multi(GatherArgs a) {
   const int lane = threadIdx.x & 31;
   const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t tend = a.tbase + a.rows * a.rb;
 
-  for (uint64_t i = warp; i < a.n; i += nwarps) {
+  for (uint64_t j = warp; j < a.n; j += nwarps) {
+    const uint64_t i = row_of<PERM>(a, j, true);
     const int64_t ridx = __ldg(a.idx + i);
     const bool ok = (uint64_t)ridx < a.rows;
     const uint64_t s = a.tbase + (ok ? (uint64_t)ridx : 0ull) * a.rb;
@@ -296,6 +309,52 @@ __global__ void __launch_bounds__(256) k_multi(GatherArgs a) {
       }
     }
     if (!ok && lane == 0) record_bad(a.err, i);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Translation-locality reorder: a counting sort of the work items by the
+// 2-MiB region (1 << shift bytes) of the table their row starts in. The visiting order changes,
+// the result does not: every work item still writes its own output row.
+__global__ void __launch_bounds__(256) k_bucket_count(GatherArgs a, int shift, uint32_t* cnt) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+    const int64_t r = __ldg(a.idx + i);
+    const uint64_t b = (uint64_t)r < a.rows ? ((uint64_t)r * a.rb) >> shift : 0ull;
+    atomicAdd(cnt + b, 1u);
+  }
+}
+
+// In-place exclusive scan of cnt[0..nb) by one block of 1024 threads.
+__global__ void __launch_bounds__(1024) k_bucket_scan(uint32_t* cnt, uint32_t nb) {
+  __shared__ uint32_t part[1024];
+  const uint32_t per = (nb + 1023) / 1024;
+  const uint32_t lo = min(nb, threadIdx.x * per), hi = min(nb, lo + per);
+  uint32_t sum = 0;
+  for (uint32_t k = lo; k < hi; ++k) sum += cnt[k];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  for (uint32_t off = 1; off < 1024; off <<= 1) {
+    uint32_t v = threadIdx.x >= off ? part[threadIdx.x - off] : 0u;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  uint32_t run = part[threadIdx.x] - sum;
+  for (uint32_t k = lo; k < hi; ++k) {
+    const uint32_t c = cnt[k];
+    cnt[k] = run;
+    run += c;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bucket_scatter(GatherArgs a, int shift, uint32_t* cursor,
+                                                        uint32_t* perm) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+    const int64_t r = __ldg(a.idx + i);
+    const uint64_t b = (uint64_t)r < a.rows ? ((uint64_t)r * a.rb) >> shift : 0ull;
+    perm[atomicAdd(cursor + b, 1u)] = (uint32_t)i;
   }
 }
 

@@ -87,6 +87,8 @@ def test_randomized_instances(pinned_pool):
         t = ut.Table(base_addr + off, rows, rb)
         try:
             assert t.info()["registered"] == 0          # adopted: already pinned
+            if rng.random() < 0.4:
+                t.set_plan("reorder=on")                # translation-locality visiting order
             plan = rng.choice(plans)
             if plan is not None:
                 try:
@@ -193,4 +195,25 @@ def test_register_adopt_and_release():
     info = ut.ut_table_get_info(t)
     assert info["registered"] == 1 and info["rows"] == 16 and info["dev_addr"] != 0
     ut.ut_release(t)
+    hb.close()
+
+
+@pytest.mark.parametrize("rb", [4, 68, 400, 512, 2408])
+def test_reorder_on_large_table(rb):
+    """3-GiB table (beyond the ~1-GiB translation reach): auto reorder on, forced off, forced on
+    must all equal the oracle, including duplicate and out-of-range indices."""
+    tbytes = 3 << 30
+    rows = tbytes // rb
+    hb = workloads.HostBuffer(rows * rb)
+    workloads.fill_table(hb.array(), rows, rb, 12, threads=0)
+    n = max(8192, min(300_000, (64 << 20) // rb))
+    idx = workloads.uniform_idx(n, rows, 13)
+    idx[::1000] = idx[7]
+    idx[17] = -2
+    idx[n - 1] = rows
+    with ut.Table(hb.addr, rows, rb) as t:
+        for mode in ["auto", "off", "on"]:
+            t.set_plan(f"reorder={mode}")
+            _gather_check(t, hb.addr, rows, rb, idx, out_off=0)
+            _gather_check(t, hb.addr, rows, rb, idx[: n // 3], out_off=4)
     hb.close()

@@ -175,3 +175,9 @@ def sampler_for(config: str, seed: int = 1, reverse_fanouts: bool = False) -> Gr
     g = ChungLuGraph(c["n_nodes"], c["n_edges"], seed=seed)
     return GraphSageSampler(g, c["batch"], c["fanouts"], seed=seed + 6,
                             reverse_fanouts=reverse_fanouts)
+
+
+def minibatch_job(args) -> np.ndarray:
+    """Picklable worker: (config, seed, batch, rank, world, reverse) -> index list."""
+    config, seed, batch, rank, world, reverse = args
+    return sampler_for(config, seed=seed, reverse_fanouts=reverse).minibatch(batch, rank, world)
