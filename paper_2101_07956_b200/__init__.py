@@ -51,7 +51,7 @@ class _Stats(ctypes.Structure):
 
 
 def _load():
-    path = _build.build()          # no-op when libut.so is up to date
+    path = os.environ.get("UT_LIB") or _build.build()   # UT_LIB: an A/B build of the same source
     L = ctypes.CDLL(path)
     vp, u64, i64p = ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int64)
     L.ut_register.restype = vp
@@ -80,7 +80,7 @@ def _load():
 
 
 _lib = _load()
-LIB_PATH = _build.LIB
+LIB_PATH = os.environ.get("UT_LIB") or _build.LIB
 
 
 def last_error() -> tuple[int, str]:

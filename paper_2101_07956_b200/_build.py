@@ -52,4 +52,4 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force=True, verbose=True)
+    build(force=True)

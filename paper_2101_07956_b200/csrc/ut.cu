@@ -41,7 +41,7 @@ int cuda_err(cudaError_t e, const char* what) {
 }
 
 // ---- plans ------------------------------------------------------------------------------------
-enum PlanKind { P_AUTO = -1, P_NARROW = 0, P_VEC16 = 1, P_VEC16X = 2, P_REALIGN = 3, P_REALIGNX = 4 };
+enum PlanKind { P_AUTO = -1, P_NARROW = 0, P_VEC16 = 1, P_VEC16X = 2, P_REALIGN = 3, P_REALIGNX = 4, P_BULK = 5 };
 
 struct Plan {
   PlanKind kind;
@@ -62,6 +62,7 @@ const char* plan_name(const Plan& p) {
       switch (p.g) { case 1: return "realign.g1"; case 2: return "realign.g2"; case 4: return "realign.g4";
                      case 8: return "realign.g8"; case 16: return "realign.g16"; default: return "realign.g32"; }
     case P_REALIGNX: return "realign.g32x";
+    case P_BULK: return "bulk";
     default: return "invalid";
   }
 }
@@ -115,6 +116,10 @@ bool choose_plan(uint64_t base, uint64_t rows, uint64_t rb, uint64_t out, PlanKi
     case P_REALIGNX:
       *p = Plan{k, 32, clip};
       return true;
+    case P_BULK:
+      if (!aligned || rb > (uint64_t)ut::kBulkMaxRow) return false;
+      *p = Plan{k, 32, false};
+      return true;
     default:
       return false;
   }
@@ -128,6 +133,7 @@ PlanKind parse_plan(const char* s, bool* ok) {
   if (!strcmp(s, "vec16x")) return P_VEC16X;
   if (!strcmp(s, "realign")) return P_REALIGN;
   if (!strcmp(s, "realignx")) return P_REALIGNX;
+  if (!strcmp(s, "bulk")) return P_BULK;
   *ok = false;
   return P_AUTO;
 }
@@ -224,9 +230,15 @@ int grid_for(K kernel, int sms, uint64_t work_warps) {
   return (int)std::max<uint64_t>(1, std::min(full, need));
 }
 
-constexpr int kU = 4;    // single-pass: row steps in flight per warp tile
-constexpr int kUx = 2;   // multi-pass: LDG.128 per lane in flight per row iteration
-constexpr int kUn = 4;   // narrow: rows per thread in flight
+#ifndef UT_KU
+#define UT_KU 4
+#endif
+#ifndef UT_KUX
+#define UT_KUX 2
+#endif
+constexpr int kU = UT_KU;    // single-pass: row steps in flight per warp tile
+constexpr int kUx = UT_KUX;  // multi-pass: LDG.128 per lane in flight per row iteration
+constexpr int kUn = 4;       // narrow: rows per thread in flight
 
 template <typename K>
 cudaError_t launch(K kernel, int grid, cudaStream_t st, const ut::GatherArgs& a) {
@@ -284,6 +296,19 @@ cudaError_t launch_plan(const Plan& p, int sms, cudaStream_t st, const ut::Gathe
       auto k = ut::k_multi<kUx, false, false, PERM>;
       return launch(k, grid_for(k, sms, a.n), st, a);
     }
+    case P_BULK: {
+      constexpr int U = 4;
+      auto k = ut::k_bulk<U, PERM>;
+      const int smem = 8 * U * (int)((a.rb + 127) & ~127ull);
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, smem);
+      if (per_sm <= 0) per_sm = 1;
+      const uint64_t tiles = (a.n + U - 1) / U;
+      const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)sms * per_sm, (tiles + 7) / 8));
+      k<<<grid, 256, smem, st>>>(a);
+      return cudaGetLastError();
+    }
     default:
       return cudaErrorInvalidValue;
   }
@@ -299,11 +324,19 @@ template <bool PERM>
 cudaError_t timed_launch(const ut_table* t, DevState* s, const Plan& p, cudaStream_t st,
                          const ut::GatherArgs& a);
 
+// Region size of the reorder buckets: 2 MiB (the translation granularity measured on this box),
+// or finer for tables that need fewer than ut::kMaxBuckets 2-MiB regions (down to 64 KiB, which
+// also helps small rows' request rate), or coarser when the table has more regions than buckets.
 int bucket_shift(uint64_t table_bytes) {
-  int shift = 21;                                   // 2-MiB regions
-  while ((table_bytes >> shift) >= 65536) ++shift;  // at most 64K buckets
+  static const int forced = [] {
+    const char* e = getenv("UT_REORDER_SHIFT");     // A/B knob
+    return (e && *e) ? atoi(e) : 0;
+  }();
+  int shift = forced ? forced : 16;
+  while (((table_bytes - 1) >> shift) + 1 > (uint64_t)ut::kMaxBuckets) ++shift;
   return shift;
 }
+
 int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n, void* out_dev,
               cudaStream_t st) {
   Plan p;
@@ -337,12 +370,13 @@ int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n
     c.n = cnt_n;
     c.out = (uint64_t)out_dev + off * t->rb;
     c.perm = perm;
-    const int grid = (int)std::min<uint64_t>((uint64_t)s->sms * 8, (cnt_n + 255) / 256);
+    const uint64_t blocks = std::min<uint64_t>((uint64_t)s->sms * 2, (cnt_n + 2047) / 2048);
+    const uint64_t per_block = (cnt_n + blocks - 1) / blocks;
     if ((e = cudaMemsetAsync(cnt, 0, nb * sizeof(uint32_t), st)) != cudaSuccess)
       return cuda_err(e, "cudaMemsetAsync(buckets)");
-    ut::k_bucket_count<<<grid, 256, 0, st>>>(c, shift, cnt);
+    ut::k_bucket_count<<<(int)blocks, 512, 0, st>>>(c, shift, nb, per_block, cnt);
     ut::k_bucket_scan<<<1, 1024, 0, st>>>(cnt, nb);
-    ut::k_bucket_scatter<<<grid, 256, 0, st>>>(c, shift, cnt, perm);
+    ut::k_bucket_scatter<<<(int)blocks, 512, 0, st>>>(c, shift, nb, per_block, cnt, perm);
     s->launches += 3;
     e = cudaGetLastError();
     if (e == cudaSuccess) e = timed_launch<true>(t, s, p, st, c);
@@ -384,7 +418,10 @@ cudaError_t timed_launch(const ut_table* t, DevState* s, const Plan& p, cudaStre
 bool want_reorder(const ut_table* t, uint64_t n) {
   if (t->reorder == 0) return false;
   if (t->reorder == 1) return true;
-  return t->bytes > (1ull << 30) && n * t->rb >= (4ull << 20) && n >= 4096;
+  if (n < 4096 || n * t->rb < (4ull << 20)) return false;
+  // beyond the ~1-GiB translation reach every row size gains; below it only small rows, whose
+  // request rate (not bytes) is the limit, gain from visiting neighbouring rows together
+  return t->bytes > (1ull << 30) || (t->rb <= 128 && t->bytes > (64ull << 20));
 }
 
 }  // namespace

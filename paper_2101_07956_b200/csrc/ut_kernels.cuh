@@ -27,6 +27,10 @@
 #pragma once
 #include <cstdint>
 
+#ifndef UT_MINB
+#define UT_MINB 1
+#endif
+
 namespace ut {
 
 struct V4 {
@@ -35,11 +39,26 @@ struct V4 {
 
 __device__ __forceinline__ V4 v4_zero() { return V4{0u, 0u, 0u, 0u}; }
 
+#ifndef UT_LDHINT
+#define UT_LDHINT 0
+#endif
+#if UT_LDHINT == 1
+#define UT_LD16 "ld.global.nc.L1::no_allocate.L2::128B.v4.u32"
+#elif UT_LDHINT == 2
+#define UT_LD16 "ld.global.nc.L1::no_allocate.L2::256B.v4.u32"
+#elif UT_LDHINT == 3
+#define UT_LD16 "ld.global.v4.u32"
+#elif UT_LDHINT == 4
+#define UT_LD16 "ld.global.nc.L1::no_allocate.L2::64B.v4.u32"
+#else
+#define UT_LD16 "ld.global.nc.L1::no_allocate.v4.u32"
+#endif
+
 // 16-B load from the device-mapped host table. Non-coherent path, no L1 allocation: the table
 // is read-only for the duration of a gather and every byte is used once per request.
 __device__ __forceinline__ V4 ld_table16(uint64_t a) {
   V4 v;
-  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+  asm(UT_LD16 " {%0, %1, %2, %3}, [%4];"
       : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
       : "l"(a));
   return v;
@@ -159,7 +178,7 @@ __device__ __forceinline__ void record_bad(unsigned long long* err, uint64_t i) 
 // ---------------------------------------------------------------------------------------------
 // narrow<T>: one thread per row, U rows per thread in flight.
 template <typename T, int U, bool PERM>
-__global__ void __launch_bounds__(256) k_narrow(GatherArgs a) {
+__global__ void __launch_bounds__(256, UT_MINB) k_narrow(GatherArgs a) {
   const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (uint64_t base = 0; base < a.n; base += nthreads * U) {
@@ -190,7 +209,7 @@ __global__ void __launch_bounds__(256) k_narrow(GatherArgs a) {
 // Single-pass kernels: G lanes per row, 32/G rows per warp step, U steps in flight per warp tile.
 // ALIGNED: base, rb, out 16-B aligned (vec16<G>); else realign<G>.
 template <int G, int U, bool ALIGNED, bool CLIP, bool PERM>
-__global__ void __launch_bounds__(256) k_single(GatherArgs a) {
+__global__ void __launch_bounds__(256, UT_MINB) k_single(GatherArgs a) {
   constexpr int RPS = 32 / G;          // rows per warp step
   constexpr int RPT = RPS * U;         // rows per warp tile
   const int lane = threadIdx.x & 31;
@@ -253,7 +272,7 @@ __global__ void __launch_bounds__(256) k_single(GatherArgs a) {
 // Multi-pass kernels: one warp per row, the row's source window starts on a 128-B line and is
 // walked 32*U chunks at a time (U LDG.128 per lane in flight).
 template <int U, bool ALIGNED, bool CLIP, bool PERM>
-__global__ void __launch_bounds__(256) k_multi(GatherArgs a) {
+__global__ void __launch_bounds__(256, UT_MINB) k_multi(GatherArgs a) {
   const int lane = threadIdx.x & 31;
   const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -313,16 +332,129 @@ __global__ void __launch_bounds__(256) k_multi(GatherArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// Translation-locality reorder: a counting sort of the work items by the
-// 2-MiB region (1 << shift bytes) of the table their row starts in. The visiting order changes,
-// the result does not: every work item still writes its own output row.
-__global__ void __launch_bounds__(256) k_bucket_count(GatherArgs a, int shift, uint32_t* cnt) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
-    const int64_t r = __ldg(a.idx + i);
-    const uint64_t b = (uint64_t)r < a.rows ? ((uint64_t)r * a.rb) >> shift : 0ull;
-    atomicAdd(cnt + b, 1u);
+// bulk<U>: the row is fetched by the TMA unit (1-D cp.async.bulk global -> shared, completion on an
+// mbarrier) instead of by LDG, then stored to HBM from shared memory. Table base, rb and out
+// 16-B aligned, rb <= kBulkMaxRow. One warp per row-slot, U rows in flight per warp.
+constexpr int kBulkMaxRow = 4096;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+
+template <int U, bool PERM>
+__global__ void __launch_bounds__(256, 1) k_bulk(GatherArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bars[8 * U];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const uint32_t rbp = (uint32_t)((a.rb + 127) & ~127ull);
+  uint8_t* my = smem + (size_t)wib * U * rbp;
+  const uint32_t bar0 = smem_u32(&bars[wib * U]);
+  if (lane == 0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8u * u) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  __syncwarp();
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t ntiles = (a.n + U - 1) / U;
+  uint32_t phase = 0;
+  for (uint64_t tile = warp; tile < ntiles; tile += nwarps) {
+    uint32_t issued = 0;
+    uint64_t rowi[U];
+    bool inb[U];
+    if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t j = tile * U + u;
+      inb[u] = j < a.n;
+      const uint64_t i = rowi[u] = row_of<PERM>(a, j, inb[u]);
+      const int64_t r = inb[u] ? __ldg(a.idx + i) : 0;
+      const bool ok = inb[u] && (uint64_t)r < a.rows;
+      if (ok) issued |= 1u << u;
+      if (lane == 0 && ok) {
+        const uint32_t bar = bar0 + 8u * u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"((uint32_t)a.rb)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(my + (size_t)u * rbp)),
+            "l"(a.tbase + (uint64_t)r * a.rb), "r"((uint32_t)a.rb), "r"(bar)
+            : "memory");
+      }
+      if (lane == 0 && inb[u] && !ok) record_bad(a.err, i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!inb[u]) continue;
+      const uint64_t d = a.out + rowi[u] * a.rb;
+      if (issued & (1u << u)) {
+        while (!mbar_try_wait(bar0 + 8u * u, phase)) {
+        }
+        for (uint32_t c = lane * 16; c < a.rb; c += 32 * 16)
+          st16(d + c, *reinterpret_cast<const V4*>(my + (size_t)u * rbp + c));
+      } else {
+        for (uint32_t c = lane * 16; c < a.rb; c += 32 * 16) st16(d + c, v4_zero());
+      }
+    }
+    // every issued barrier completed one phase; barriers not issued stay in the old phase, so
+    // re-align them by arriving once (count 1) to keep one phase bit for all slots.
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (!(issued & (1u << u)))
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar0 + 8u * u) : "memory");
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!(issued & (1u << u))) {
+        while (!mbar_try_wait(bar0 + 8u * u, phase)) {
+        }
+      }
+    }
+    phase ^= 1u;
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Translation-locality reorder: a counting sort of the work items by the table
+// region (1 << shift bytes, at most kMaxBuckets regions) their row starts in. The visiting order
+// changes, the result does not: every work item still writes its own output row.
+// Each block owns a contiguous chunk of work items and keeps a shared-memory histogram, so global
+// atomics are one per (block, non-empty bucket) instead of one per item.
+constexpr int kMaxBuckets = 8192;
+
+__device__ __forceinline__ uint32_t bucket_of(const GatherArgs& a, uint64_t i, int shift) {
+  const int64_t r = __ldg(a.idx + i);
+  return (uint64_t)r < a.rows ? (uint32_t)(((uint64_t)r * a.rb) >> shift) : 0u;
+}
+
+__global__ void __launch_bounds__(512) k_bucket_count(GatherArgs a, int shift, uint32_t nb,
+                                                      uint64_t chunk, uint32_t* cnt) {
+  __shared__ uint32_t hist[kMaxBuckets];
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
+  __syncthreads();
+  const uint64_t lo = (uint64_t)blockIdx.x * chunk;
+  const uint64_t hi = min(a.n, lo + chunk);
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(&hist[bucket_of(a, i, shift)], 1u);
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x)
+    if (hist[b]) atomicAdd(cnt + b, hist[b]);
 }
 
 // In-place exclusive scan of cnt[0..nb) by one block of 1024 threads.
@@ -348,14 +480,24 @@ __global__ void __launch_bounds__(1024) k_bucket_scan(uint32_t* cnt, uint32_t nb
   }
 }
 
-__global__ void __launch_bounds__(256) k_bucket_scatter(GatherArgs a, int shift, uint32_t* cursor,
+__global__ void __launch_bounds__(512) k_bucket_scatter(GatherArgs a, int shift, uint32_t nb,
+                                                        uint64_t chunk, uint32_t* cursor,
                                                         uint32_t* perm) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
-    const int64_t r = __ldg(a.idx + i);
-    const uint64_t b = (uint64_t)r < a.rows ? ((uint64_t)r * a.rb) >> shift : 0ull;
-    perm[atomicAdd(cursor + b, 1u)] = (uint32_t)i;
+  __shared__ uint32_t hist[kMaxBuckets];
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
+  __syncthreads();
+  const uint64_t lo = (uint64_t)blockIdx.x * chunk;
+  const uint64_t hi = min(a.n, lo + chunk);
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(&hist[bucket_of(a, i, shift)], 1u);
+  __syncthreads();
+  // reserve this block's range in every non-empty bucket; hist[b] becomes the range start
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
+    const uint32_t c = hist[b];
+    if (c) hist[b] = atomicAdd(cursor + b, c);
   }
+  __syncthreads();
+  for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
+    perm[atomicAdd(&hist[bucket_of(a, i, shift)], 1u)] = (uint32_t)i;
 }
 
 }  // namespace ut
