@@ -111,8 +111,8 @@ class Dist:
             import torch.distributed as td
             if backend == "nccl":
                 import torch
-                torch.cuda.set_device(self.local_rank)
-                td.init_process_group(backend="nccl", device_id=torch.device("cuda", self.local_rank))
+                torch.cuda.set_device(self.local_rank % torch.cuda.device_count())
+                td.init_process_group(backend="nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
             else:
                 td.init_process_group(backend=backend)
             self.pg = td
@@ -137,6 +137,14 @@ class Dist:
     def close(self):
         if self.pg is not None:
             self.pg.destroy_process_group()
+
+
+def box_throughput(dist, nbytes: int, dev_ms: float, wall_s: float, launches: int):
+    """Whole-box GB/s = (sum over ranks of useful bytes) / (max over ranks of device time).
+    Returns (GB/s, max device ms, max wall s, total launches)."""
+    max_dev_ms, max_wall = dist.allreduce([dev_ms, wall_s], "max")
+    box_bytes, total_launches = dist.allreduce([float(nbytes), float(launches)], "sum")
+    return box_bytes / (max_dev_ms / 1e3) / 1e9, max_dev_ms, max_wall, int(total_launches)
 
 
 # ---- measurement helpers -----------------------------------------------------------------------
@@ -294,7 +302,8 @@ def run_ut(args, spec, dist):
     procs = max(1, (os.cpu_count() or 1) // world)
     lists = make_index_lists(spec, rank, world, count, seed + 17, procs)   # before CUDA init
 
-    torch.cuda.set_device(dist.local_rank)
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(dist.local_rank % ndev)     # > 1 rank per GPU only with --backend gloo
     dist.init(args.backend)
     import paper_2101_07956_b200 as ut
 
@@ -330,7 +339,7 @@ def run_ut(args, spec, dist):
         if not parity:
             raise SystemExit(f"rank {rank}: parity failure on minibatch 0")
 
-    clocks = ClockSampler(dist.local_rank)
+    clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
     # warm-up
     for s in range(args.warmup):
@@ -363,11 +372,8 @@ def run_ut(args, spec, dist):
     table.set_plan("timing=off")
     dev_ms = sum(a.elapsed_time(b) for a, b in evs)
 
-    red = dist.allreduce([dev_ms, wall], "max")
-    tot = dist.allreduce([float(nbytes), float(st["kernel_launches"])], "sum")
-    max_dev_ms, max_wall = red
-    box_bytes, launches = tot
-    value = box_bytes / (max_dev_ms / 1e3) / 1e9
+    value, max_dev_ms, max_wall, launches = box_throughput(dist, nbytes, dev_ms, wall,
+                                                           st["kernel_launches"])
     per_gpu = nbytes / (dev_ms / 1e3) / 1e9
     kern_ms = st["gather_kernel_ms"] / max(1, st["timed_launches"])
     kern_bytes = nbytes / max(1, st["timed_launches"])
@@ -395,7 +401,7 @@ def run_ut(args, spec, dist):
         e_tot = dist.allreduce([float(e_bytes)], "sum")[0]
         e2e = {"value": round(e_tot / mx / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps),
-               "path": "ut_gather_host: idx H2D + gather + rows D2H, chunked on two streams"}
+               "path": "ut_gather_host: idx H2D copy, then the gather kernel stores rows into pinned host memory"}
         del out_host, idx_host
 
     # context baselines on rank 0 at N=1: the oracle and the paper's CPU-centric path
@@ -427,6 +433,7 @@ def run_ut(args, spec, dist):
                          "peak_source": "pinned cudaMemcpy H2D measured in this run (best of 10 x 1 GiB)"},
             "cpu_baseline": cpu_base, "py_baseline": py_base, "e2e": e2e,
             "gpu_launches": n_launch, "clocks": clk,
+            "ranks_per_gpu": max(1, world // max(1, torch.cuda.device_count())),
             "parity_checked": parity, "register_s": round(reg_s, 3),
             "wall_ms_per_step": round(max_wall / args.steps * 1e3, 3),
         }

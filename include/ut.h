@@ -100,14 +100,16 @@ UT_API int ut_gather(const ut_table* t, const int64_t* idx_dev, uint64_t n, void
               ut_stream_t stream);
 
 /*
- * ut_gather_host — the same gather from and to HOST buffers (the end-to-end form): copies
- * idx_host to the device, gathers, and copies the rows back to out_host, pipelined in chunks
- * on `stream` plus one library-owned copy stream so that the link's two directions overlap.
+ * ut_gather_host — the same gather from and to HOST buffers (the end-to-end form).
  *   idx_host  n int64 row ids in host memory (page-locked for full speed; caller-owned).
- *   out_host  >= n*rb bytes of host memory (page-locked for full speed; caller-owned).
- * Device scratch (two chunks of idx and rows) is owned by the table and grown on demand.
- * Synchronous: returns after out_host holds the result. Out-of-range handling as ut_gather.
- * Returns UT_OK, UT_EINVAL, UT_ENOMEM or UT_ECUDA.
+ *   out_host  >= n*rb bytes of host memory (caller-owned).
+ * If out_host is page-locked and mapped (cudaHostAlloc / cudaHostRegister'ed), idx is copied to
+ * the device and the gather kernel stores the rows straight into out_host over the link (one
+ * pass, no HBM round trip). Otherwise rows are gathered in chunks into library-owned device
+ * scratch and copied back by the copy engine on a second stream, overlapping the two link
+ * directions (UT_HOST_PIPELINE=1 forces this path). Device scratch is owned by the table and
+ * grown on demand. Synchronous: returns after out_host holds the result, on `stream`.
+ * Out-of-range handling as ut_gather. Returns UT_OK, UT_EINVAL, UT_ENOMEM or UT_ECUDA.
  */
 UT_API int ut_gather_host(const ut_table* t, const int64_t* idx_host, uint64_t n, void* out_host,
                    ut_stream_t stream);

@@ -158,6 +158,8 @@ struct DevState {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t gathered[kBuf] = {};
   cudaEvent_t drained[kBuf] = {};
+  int64_t* idx_all = nullptr;           // ut_gather_host zero-copy path: device copy of idx
+  uint64_t idx_cap = 0;
 };
 
 }  // namespace
@@ -533,10 +535,46 @@ int ut_gather_host(const ut_table* ct, const int64_t* idx_host, uint64_t n, void
   if (rc != UT_OK) return rc;
   std::lock_guard<std::mutex> lk(t->mu);
   cudaStream_t st = (cudaStream_t)stream;
-  const uint64_t chunk_bytes = 8ull << 20;
+  cudaError_t e;
+  // Fast path: out_host is page-locked and mapped, so the gather kernel stores the rows straight
+  // into it over the link (one pass, no HBM round trip, no copy engine); the index list is copied
+  // to the device once (8 B/row) so the kernel's reads on the link are table rows only.
+  cudaPointerAttributes oa{};
+  void* out_mapped = nullptr;
+  if (cudaPointerGetAttributes(&oa, out_host) == cudaSuccess && oa.type == cudaMemoryTypeHost &&
+      oa.devicePointer != nullptr) {
+    cudaPointerAttributes ea{};
+    const uint8_t* last = (const uint8_t*)out_host + n * t->rb - 1;
+    if (cudaPointerGetAttributes(&ea, last) == cudaSuccess && ea.type == cudaMemoryTypeHost)
+      out_mapped = oa.devicePointer;
+  }
+  cudaGetLastError();
+  if (out_mapped && !getenv("UT_HOST_PIPELINE")) {
+    if (s->idx_cap < n) {
+      if (s->idx_all) cudaFree(s->idx_all);
+      s->idx_all = nullptr;
+      s->idx_cap = 0;
+      if (cudaMalloc(&s->idx_all, n * sizeof(int64_t)) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(UT_ENOMEM, "device index scratch of %llu rows", (unsigned long long)n);
+      }
+      s->idx_cap = n;
+    }
+    if ((e = cudaMemcpyAsync(s->idx_all, idx_host, n * sizeof(int64_t), cudaMemcpyHostToDevice,
+                             st)) != cudaSuccess)
+      return cuda_err(e, "cudaMemcpyAsync(idx H2D)");
+    if ((rc = gather_on(t, s, s->idx_all, n, out_mapped, st)) != UT_OK) return rc;
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_err(e, "sync stream");
+    return UT_OK;
+  }
+  // Otherwise: chunks of rows gathered into device scratch and copied back by the copy engine
+  // on a second stream, so the link's two directions overlap.
+  static const uint64_t chunk_bytes = [] {
+    const char* e = getenv("UT_HOST_CHUNK");          // A/B knob (bytes of rows per chunk)
+    return (e && *e) ? (uint64_t)atoll(e) : (8ull << 20);
+  }();
   const uint64_t chunk = std::max<uint64_t>(1, chunk_bytes / t->rb);
   const uint64_t want = std::min<uint64_t>(chunk, n);
-  cudaError_t e;
   if (s->buf_rows < want) {
     for (int b = 0; b < DevState::kBuf; ++b) {
       cudaFree(s->idx_buf[b]);
@@ -601,6 +639,7 @@ int ut_release(ut_table* t) {
       if (s.drained[b]) cudaEventDestroy(s.drained[b]);
     }
     if (s.copy_stream) cudaStreamDestroy(s.copy_stream);
+    if (s.idx_all) cudaFree(s.idx_all);
     for (auto* v : {&s.pending, &s.spare})
       for (auto& ev : *v) {
         cudaEventDestroy(ev.first);

@@ -168,16 +168,23 @@ def test_other_stream_and_consumer_ordering(rb):
 
 
 @pytest.mark.parametrize("rb", [4, 68, 400, 2052])
-def test_gather_host_end_to_end(rb):
+@pytest.mark.parametrize("path", ["zero-copy", "pipeline", "pageable"])
+def test_gather_host_end_to_end(rb, path, monkeypatch):
     rows = 300_000 if rb < 1000 else 30_000
     hb = workloads.HostBuffer(rows * rb, offset=rb % 7)
     workloads.fill_table(hb.array(), rows, rb, 10)
     idx = workloads.uniform_idx(123_457, rows, 11)
     idx[5] = rows + 3
     want, bad = oracle.gather(hb.addr, rows, rb, idx)
+    if path == "pipeline":
+        monkeypatch.setenv("UT_HOST_PIPELINE", "1")
     with ut.Table(hb.addr, rows, rb) as t:
         idx_h = torch.from_numpy(idx).pin_memory()
-        out = t.gather_host(idx_h)
+        if path == "pageable":
+            out = torch.full((idx.size, rb), SENT, dtype=torch.uint8)
+            t.gather_host(idx_h, out_host=out)
+        else:
+            out = t.gather_host(idx_h)
         assert out.numpy().tobytes() == want.tobytes()
         assert t.error_pos() == bad == 5
     hb.close()
