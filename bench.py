@@ -301,6 +301,8 @@ def run_ut(args, spec, dist):
     count = min(args.warmup + args.steps, args.max_lists)
     procs = max(1, (os.cpu_count() or 1) // world)
     lists = make_index_lists(spec, rank, world, count, seed + 17, procs)   # before CUDA init
+    if args.presort:   # experiment only: what a perfectly address-ordered list would give
+        lists = [np.sort(l) for l in lists]
 
     ndev = torch.cuda.device_count()
     torch.cuda.set_device(dist.local_rank % ndev)     # > 1 rank per GPU only with --backend gloo
@@ -487,6 +489,7 @@ def main(argv=None):
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", dest="check", action="store_false")
     ap.add_argument("--backend", default="nccl", help="process-group backend at N > 1")
+    ap.add_argument("--presort", action="store_true", help="experiment: sort index lists on the host")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")

@@ -154,6 +154,9 @@ UT_API const char* ut_plan_probe(uint64_t base, uint64_t rows, uint64_t row_byte
  * the table violates returns UT_EINVAL and leaves the plan unchanged; every admissible kind is
  * correct for any output alignment (ut_gather falls back to "auto" for an output it cannot take).
  * "timing=on|off" brackets each gather-kernel launch with CUDA events (see ut_get_stats).
+ * "conc=auto|dense|sparse" picks the launch shape: dense = every SM full of warps; sparse = a
+ * quarter of the SMs, one row-step per warp (fewer translation pages in flight); auto = sparse
+ * for reordered gathers from tables > 1 GiB.
  * "reorder=on|off|auto" controls the translation-locality stage instead:
  * work items are visited grouped by the 2-MiB table region their row lies in, the output order
  * is unchanged; "auto" enables it for tables > 1 GiB and gathers of >= 4 MiB.

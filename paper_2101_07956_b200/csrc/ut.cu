@@ -173,6 +173,7 @@ struct ut_table {
   PlanKind forced = P_AUTO;
   int reorder = -1;                     // -1 auto, 0 off, 1 on (ut_set_plan "reorder=...")
   bool timing = false;                  // ut_set_plan "timing=on"
+  int conc = -1;                        // launch shape: -1 auto, 0 dense, 1 sparse ("conc=...")
   std::mutex mu;
   DevState dev[kMaxDev];
 };
@@ -222,12 +223,27 @@ int dev_state(const ut_table* ct, DevState** out) {
   return UT_OK;
 }
 
+int blocks_per_sm_cap() {
+  static const int cap = [] {
+    const char* e = getenv("UT_BLOCKS_PER_SM");     // A/B knob: cap resident gather blocks per SM
+    return (e && *e) ? atoi(e) : 0;
+  }();
+  return cap;
+}
+
 template <typename K>
-int grid_for(K kernel, int sms, uint64_t work_warps) {
+int grid_for(K kernel, int sms, uint64_t work_warps, int cap_blocks = 0) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
   if (per_sm <= 0) per_sm = 1;
+  if (blocks_per_sm_cap() > 0) per_sm = std::min(per_sm, blocks_per_sm_cap());
   uint64_t full = (uint64_t)sms * per_sm;
+  static const int max_blocks = [] {
+    const char* e = getenv("UT_MAX_BLOCKS");        // A/B knob: cap the gather grid
+    return (e && *e) ? atoi(e) : 0;
+  }();
+  if (max_blocks > 0) full = std::min<uint64_t>(full, (uint64_t)max_blocks);
+  if (cap_blocks > 0) full = std::min<uint64_t>(full, (uint64_t)cap_blocks);
   uint64_t need = (work_warps + 7) / 8;
   return (int)std::max<uint64_t>(1, std::min(full, need));
 }
@@ -248,55 +264,75 @@ cudaError_t launch(K kernel, int grid, cudaStream_t st, const ut::GatherArgs& a)
   return cudaGetLastError();
 }
 
-template <int G, bool PERM>
-cudaError_t launch_single(const Plan& p, int sms, cudaStream_t st, const ut::GatherArgs& a) {
-  constexpr uint64_t rpt = (32 / G) * kU;
+// Launch shape. "dense": every SM full of warps, U row-steps in flight per warp — right while the
+// table fits the translation reach. "sparse" (reordered gathers from tables beyond the reach):
+// one row-step per warp on a quarter of the SMs (~300 rows, ~150-300 KB in flight — enough for
+// the link's bandwidth x loaded latency of ~3.7 us), because more rows in flight touch more
+// translation pages at once and lose more than they hide (measured sweep).
+struct Shape {
+  bool sparse;
+  int cap_blocks;
+};
+
+template <int G, int U, bool PERM>
+cudaError_t launch_single_u(const Plan& p, int sms, cudaStream_t st, const ut::GatherArgs& a,
+                            int cap) {
+  constexpr uint64_t rpt = (32 / G) * U;
   const uint64_t tiles = (a.n + rpt - 1) / rpt;
   if (p.kind == P_VEC16) {
-    auto k = ut::k_single<G, kU, true, false, PERM>;
-    return launch(k, grid_for(k, sms, tiles), st, a);
+    auto k = ut::k_single<G, U, true, false, PERM>;
+    return launch(k, grid_for(k, sms, tiles, cap), st, a);
   }
   if (p.clip) {
-    auto k = ut::k_single<G, kU, false, true, PERM>;
-    return launch(k, grid_for(k, sms, tiles), st, a);
+    auto k = ut::k_single<G, U, false, true, PERM>;
+    return launch(k, grid_for(k, sms, tiles, cap), st, a);
   }
-  auto k = ut::k_single<G, kU, false, false, PERM>;
-  return launch(k, grid_for(k, sms, tiles), st, a);
+  auto k = ut::k_single<G, U, false, false, PERM>;
+  return launch(k, grid_for(k, sms, tiles, cap), st, a);
+}
+
+template <int G, bool PERM>
+cudaError_t launch_single(const Plan& p, int sms, cudaStream_t st, const ut::GatherArgs& a,
+                          const Shape& sh) {
+  if (PERM && sh.sparse) return launch_single_u<G, 1, PERM>(p, sms, st, a, sh.cap_blocks);
+  return launch_single_u<G, kU, PERM>(p, sms, st, a, 0);
 }
 
 template <bool PERM>
-cudaError_t launch_plan(const Plan& p, int sms, cudaStream_t st, const ut::GatherArgs& a) {
+cudaError_t launch_plan(const Plan& p, int sms, cudaStream_t st, const ut::GatherArgs& a,
+                        const Shape& sh) {
+  const int cap = sh.sparse ? sh.cap_blocks : 0;
   switch (p.kind) {
     case P_NARROW: {
       const uint64_t warps = (a.n + 32 * kUn - 1) / (32 * kUn);
       switch (p.g) {
-        case 1: { auto k = ut::k_narrow<uint8_t, kUn, PERM>; return launch(k, grid_for(k, sms, warps), st, a); }
-        case 2: { auto k = ut::k_narrow<uint16_t, kUn, PERM>; return launch(k, grid_for(k, sms, warps), st, a); }
-        case 4: { auto k = ut::k_narrow<uint32_t, kUn, PERM>; return launch(k, grid_for(k, sms, warps), st, a); }
-        default: { auto k = ut::k_narrow<uint64_t, kUn, PERM>; return launch(k, grid_for(k, sms, warps), st, a); }
+        case 1: { auto k = ut::k_narrow<uint8_t, kUn, PERM>; return launch(k, grid_for(k, sms, warps, cap), st, a); }
+        case 2: { auto k = ut::k_narrow<uint16_t, kUn, PERM>; return launch(k, grid_for(k, sms, warps, cap), st, a); }
+        case 4: { auto k = ut::k_narrow<uint32_t, kUn, PERM>; return launch(k, grid_for(k, sms, warps, cap), st, a); }
+        default: { auto k = ut::k_narrow<uint64_t, kUn, PERM>; return launch(k, grid_for(k, sms, warps, cap), st, a); }
       }
     }
     case P_VEC16:
     case P_REALIGN:
       switch (p.g) {
-        case 1: return launch_single<1, PERM>(p, sms, st, a);
-        case 2: return launch_single<2, PERM>(p, sms, st, a);
-        case 4: return launch_single<4, PERM>(p, sms, st, a);
-        case 8: return launch_single<8, PERM>(p, sms, st, a);
-        case 16: return launch_single<16, PERM>(p, sms, st, a);
-        default: return launch_single<32, PERM>(p, sms, st, a);
+        case 1: return launch_single<1, PERM>(p, sms, st, a, sh);
+        case 2: return launch_single<2, PERM>(p, sms, st, a, sh);
+        case 4: return launch_single<4, PERM>(p, sms, st, a, sh);
+        case 8: return launch_single<8, PERM>(p, sms, st, a, sh);
+        case 16: return launch_single<16, PERM>(p, sms, st, a, sh);
+        default: return launch_single<32, PERM>(p, sms, st, a, sh);
       }
     case P_VEC16X: {
       auto k = ut::k_multi<kUx, true, false, PERM>;
-      return launch(k, grid_for(k, sms, a.n), st, a);
+      return launch(k, grid_for(k, sms, a.n, cap), st, a);
     }
     case P_REALIGNX: {
       if (p.clip) {
         auto k = ut::k_multi<kUx, false, true, PERM>;
-        return launch(k, grid_for(k, sms, a.n), st, a);
+        return launch(k, grid_for(k, sms, a.n, cap), st, a);
       }
       auto k = ut::k_multi<kUx, false, false, PERM>;
-      return launch(k, grid_for(k, sms, a.n), st, a);
+      return launch(k, grid_for(k, sms, a.n, cap), st, a);
     }
     case P_BULK: {
       constexpr int U = 4;
@@ -324,23 +360,25 @@ bool want_reorder(const ut_table* t, uint64_t n);
 
 template <bool PERM>
 cudaError_t timed_launch(const ut_table* t, DevState* s, const Plan& p, cudaStream_t st,
-                         const ut::GatherArgs& a);
+                         const ut::GatherArgs& a, bool host_out);
+Shape shape_for(const ut_table* t, const DevState* s, bool reordered, uint64_t n, bool host_out);
 
-// Region size of the reorder buckets: 2 MiB (the translation granularity measured on this box),
-// or finer for tables that need fewer than ut::kMaxBuckets 2-MiB regions (down to 64 KiB, which
-// also helps small rows' request rate), or coarser when the table has more regions than buckets.
-int bucket_shift(uint64_t table_bytes) {
+// Region size of the reorder buckets. Rows > 128 B on tables beyond the translation reach:
+// 2-MiB regions (the granularity that restores link speed). Rows <= 128 B, whose
+// request rate also gains from visiting neighbouring lines together: 64-KiB regions. Either is
+// coarsened until the table has at most ut::kMaxBuckets regions (fewer buckets = fewer atomics).
+int bucket_shift(uint64_t table_bytes, uint64_t rb) {
   static const int forced = [] {
     const char* e = getenv("UT_REORDER_SHIFT");     // A/B knob
     return (e && *e) ? atoi(e) : 0;
   }();
-  int shift = forced ? forced : 16;
+  int shift = forced ? forced : (rb > 128 && table_bytes > (1ull << 30)) ? 21 : 16;
   while (((table_bytes - 1) >> shift) + 1 > (uint64_t)ut::kMaxBuckets) ++shift;
   return shift;
 }
 
 int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n, void* out_dev,
-              cudaStream_t st) {
+              cudaStream_t st, bool host_out = false) {
   Plan p;
   if (!choose_plan((uint64_t)t->host, t->rows, t->rb, (uint64_t)out_dev, t->forced, &p) &&
       !choose_plan((uint64_t)t->host, t->rows, t->rb, (uint64_t)out_dev, P_AUTO, &p))
@@ -350,13 +388,13 @@ int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n
   s->rows += n;
   s->bytes += n * t->rb;
   if (!want_reorder(t, n)) {
-    e = timed_launch<false>(t, s, p, st, a);
+    e = timed_launch<false>(t, s, p, st, a, host_out);
     if (e != cudaSuccess) return cuda_err(e, plan_name(p));
     return UT_OK;
   }
   // counting sort of the work items by 2-MiB table region (stream-ordered scratch from the
   // library's pool); n < 2^32 per launch, larger gathers are split.
-  const int shift = bucket_shift(t->bytes);
+  const int shift = bucket_shift(t->bytes, t->rb);
   const uint32_t nb = (uint32_t)(((t->bytes - 1) >> shift) + 1);
   const uint64_t chunk = 1ull << 31;
   for (uint64_t off = 0; off < n; off += chunk) {
@@ -376,12 +414,20 @@ int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n
     const uint64_t per_block = (cnt_n + blocks - 1) / blocks;
     if ((e = cudaMemsetAsync(cnt, 0, nb * sizeof(uint32_t), st)) != cudaSuccess)
       return cuda_err(e, "cudaMemsetAsync(buckets)");
-    ut::k_bucket_count<<<(int)blocks, 512, 0, st>>>(c, shift, nb, per_block, cnt);
-    ut::k_bucket_scan<<<1, 1024, 0, st>>>(cnt, nb);
-    ut::k_bucket_scatter<<<(int)blocks, 512, 0, st>>>(c, shift, nb, per_block, cnt, perm);
+    const int hsm = (int)(nb * sizeof(uint32_t));
+    static const bool smem_ok = [] {
+      const int mx = ut::kMaxBuckets * (int)sizeof(uint32_t);
+      return cudaFuncSetAttribute(ut::k_bucket_count, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess &&
+             cudaFuncSetAttribute(ut::k_bucket_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess &&
+             cudaFuncSetAttribute(ut::k_bucket_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess;
+    }();
+    if (!smem_ok) return set_err(UT_ECUDA, "cannot opt in to %d B of shared memory", hsm);
+    ut::k_bucket_count<<<(int)blocks, 512, hsm, st>>>(c, shift, nb, per_block, cnt);
+    ut::k_bucket_scan<<<1, 1024, hsm, st>>>(cnt, nb);
+    ut::k_bucket_scatter<<<(int)blocks, 512, hsm, st>>>(c, shift, nb, per_block, cnt, perm);
     s->launches += 3;
     e = cudaGetLastError();
-    if (e == cudaSuccess) e = timed_launch<true>(t, s, p, st, c);
+    if (e == cudaSuccess) e = timed_launch<true>(t, s, p, st, c, host_out);
     cudaError_t e2 = cudaFreeAsync(scratch, st);
     if (e != cudaSuccess) return cuda_err(e, plan_name(p));
     if (e2 != cudaSuccess) return cuda_err(e2, "cudaFreeAsync(reorder scratch)");
@@ -391,7 +437,7 @@ int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n
 
 template <bool PERM>
 cudaError_t timed_launch(const ut_table* t, DevState* s, const Plan& p, cudaStream_t st,
-                         const ut::GatherArgs& a) {
+                         const ut::GatherArgs& a, bool host_out) {
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
   if (t->timing) {
     std::lock_guard<std::mutex> lk(s->tmu);
@@ -404,7 +450,7 @@ cudaError_t timed_launch(const ut_table* t, DevState* s, const Plan& p, cudaStre
     }
     cudaEventRecord(ev.first, st);
   }
-  cudaError_t e = launch_plan<PERM>(p, s->sms, st, a);
+  cudaError_t e = launch_plan<PERM>(p, s->sms, st, a, shape_for(t, s, PERM, a.n, host_out));
   if (e == cudaSuccess) {
     s->gathers += 1;
     s->launches += 1;
@@ -415,6 +461,22 @@ cudaError_t timed_launch(const ut_table* t, DevState* s, const Plan& p, cudaStre
     s->pending.push_back(ev);
   }
   return e;
+}
+
+Shape shape_for(const ut_table* t, const DevState* s, bool reordered, uint64_t n, bool host_out) {
+  static const int env_blocks = [] {
+    const char* e = getenv("UT_SPARSE_BLOCKS");     // A/B knob: grid of the sparse shape
+    return (e && *e) ? atoi(e) : 0;
+  }();
+  // sparse when the gather brings few bytes per 2-MiB table region: each region's translation is
+  // then amortised over little data, and fewer regions in flight is what keeps the link busy
+  const uint64_t regions = std::min<uint64_t>(n, ((t->bytes - 1) >> 21) + 1);
+  const bool thin = n * t->rb < (32ull << 10) * regions;
+  // stores into mapped host memory add their own latency to every row: keep the dense shape there
+  bool sparse = t->conc == 1 ||
+                (t->conc == -1 && reordered && !host_out && t->bytes > (1ull << 30) && thin);
+  int cap = env_blocks > 0 ? env_blocks : std::max(1, s->sms / 4);
+  return Shape{sparse, cap};
 }
 
 bool want_reorder(const ut_table* t, uint64_t n) {
@@ -563,7 +625,7 @@ int ut_gather_host(const ut_table* ct, const int64_t* idx_host, uint64_t n, void
     if ((e = cudaMemcpyAsync(s->idx_all, idx_host, n * sizeof(int64_t), cudaMemcpyHostToDevice,
                              st)) != cudaSuccess)
       return cuda_err(e, "cudaMemcpyAsync(idx H2D)");
-    if ((rc = gather_on(t, s, s->idx_all, n, out_mapped, st)) != UT_OK) return rc;
+    if ((rc = gather_on(t, s, s->idx_all, n, out_mapped, st, true)) != UT_OK) return rc;
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_err(e, "sync stream");
     return UT_OK;
   }
@@ -708,6 +770,14 @@ int ut_set_plan(ut_table* t, const char* name) {
   if (!t || !name) return set_err(UT_EINVAL, "NULL argument");
   if (!strcmp(name, "timing=on") || !strcmp(name, "timing=off")) {
     t->timing = name[8] == 'n';
+    return UT_OK;
+  }
+  if (!strncmp(name, "conc=", 5)) {
+    const char* v = name + 5;
+    if (!strcmp(v, "auto")) t->conc = -1;
+    else if (!strcmp(v, "dense")) t->conc = 0;
+    else if (!strcmp(v, "sparse")) t->conc = 1;
+    else return set_err(UT_EINVAL, "conc must be auto|dense|sparse, got '%s'", v);
     return UT_OK;
   }
   if (!strncmp(name, "reorder=", 8)) {

@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(256, 1) k_bulk(GatherArgs a) {
 // changes, the result does not: every work item still writes its own output row.
 // Each block owns a contiguous chunk of work items and keeps a shared-memory histogram, so global
 // atomics are one per (block, non-empty bucket) instead of one per item.
-constexpr int kMaxBuckets = 8192;
+constexpr int kMaxBuckets = 32768;   // 128 KiB of dynamic shared memory per block
 
 __device__ __forceinline__ uint32_t bucket_of(const GatherArgs& a, uint64_t i, int shift) {
   const int64_t r = __ldg(a.idx + i);
@@ -446,7 +446,7 @@ __device__ __forceinline__ uint32_t bucket_of(const GatherArgs& a, uint64_t i, i
 
 __global__ void __launch_bounds__(512) k_bucket_count(GatherArgs a, int shift, uint32_t nb,
                                                       uint64_t chunk, uint32_t* cnt) {
-  __shared__ uint32_t hist[kMaxBuckets];
+  extern __shared__ uint32_t hist[];    // nb entries
   for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
   __syncthreads();
   const uint64_t lo = (uint64_t)blockIdx.x * chunk;
@@ -457,33 +457,40 @@ __global__ void __launch_bounds__(512) k_bucket_count(GatherArgs a, int shift, u
     if (hist[b]) atomicAdd(cnt + b, hist[b]);
 }
 
-// In-place exclusive scan of cnt[0..nb) by one block of 1024 threads.
+// In-place exclusive scan of cnt[0..nb) by one block of 1024 threads: the counts are staged in
+// shared memory with coalesced loads, each thread scans a contiguous run, runs are combined with
+// a block-wide scan, and the result is written back coalesced.
 __global__ void __launch_bounds__(1024) k_bucket_scan(uint32_t* cnt, uint32_t nb) {
+  extern __shared__ uint32_t v[];       // nb entries
   __shared__ uint32_t part[1024];
+  for (uint32_t k = threadIdx.x; k < nb; k += 1024) v[k] = cnt[k];
+  __syncthreads();
   const uint32_t per = (nb + 1023) / 1024;
   const uint32_t lo = min(nb, threadIdx.x * per), hi = min(nb, lo + per);
   uint32_t sum = 0;
-  for (uint32_t k = lo; k < hi; ++k) sum += cnt[k];
+  for (uint32_t k = lo; k < hi; ++k) sum += v[k];
   part[threadIdx.x] = sum;
   __syncthreads();
   for (uint32_t off = 1; off < 1024; off <<= 1) {
-    uint32_t v = threadIdx.x >= off ? part[threadIdx.x - off] : 0u;
+    uint32_t x = threadIdx.x >= off ? part[threadIdx.x - off] : 0u;
     __syncthreads();
-    part[threadIdx.x] += v;
+    part[threadIdx.x] += x;
     __syncthreads();
   }
   uint32_t run = part[threadIdx.x] - sum;
   for (uint32_t k = lo; k < hi; ++k) {
-    const uint32_t c = cnt[k];
-    cnt[k] = run;
+    const uint32_t c = v[k];
+    v[k] = run;
     run += c;
   }
+  __syncthreads();
+  for (uint32_t k = threadIdx.x; k < nb; k += 1024) cnt[k] = v[k];
 }
 
 __global__ void __launch_bounds__(512) k_bucket_scatter(GatherArgs a, int shift, uint32_t nb,
                                                         uint64_t chunk, uint32_t* cursor,
                                                         uint32_t* perm) {
-  __shared__ uint32_t hist[kMaxBuckets];
+  extern __shared__ uint32_t hist[];    // nb entries
   for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
   __syncthreads();
   const uint64_t lo = (uint64_t)blockIdx.x * chunk;

@@ -10,7 +10,7 @@ VARIANTS = {
     "base": [],
     "l2_64": ["-DUT_LDHINT=4"], "l2_128": ["-DUT_LDHINT=1"], "l2_256": ["-DUT_LDHINT=2"],
     "ldplain": ["-DUT_LDHINT=3"],
-    "ku2": ["-DUT_KU=2"], "ku8": ["-DUT_KU=8"], "kux1": ["-DUT_KUX=1"], "kux4": ["-DUT_KUX=4"],
+    "ku1": ["-DUT_KU=1"], "ku2": ["-DUT_KU=2"], "ku8": ["-DUT_KU=8"], "kux1": ["-DUT_KUX=1"], "kux4": ["-DUT_KUX=4"],
     "minb6": ["-DUT_MINB=6"], "minb8": ["-DUT_MINB=8"],
 }
 

@@ -89,6 +89,7 @@ def test_randomized_instances(pinned_pool):
             assert t.info()["registered"] == 0          # adopted: already pinned
             if rng.random() < 0.4:
                 t.set_plan("reorder=on")                # translation-locality visiting order
+            t.set_plan("conc=" + rng.choice(["auto", "dense", "sparse"]))   # launch shape
             plan = rng.choice(plans)
             if plan is not None:
                 try:
@@ -219,8 +220,9 @@ def test_reorder_on_large_table(rb):
     idx[17] = -2
     idx[n - 1] = rows
     with ut.Table(hb.addr, rows, rb) as t:
-        for mode in ["auto", "off", "on"]:
+        for mode, conc in [("auto", "auto"), ("off", "dense"), ("on", "sparse"), ("on", "dense")]:
             t.set_plan(f"reorder={mode}")
+            t.set_plan(f"conc={conc}")
             _gather_check(t, hb.addr, rows, rb, idx, out_off=0)
             _gather_check(t, hb.addr, rows, rb, idx[: n // 3], out_off=4)
     hb.close()
