@@ -41,7 +41,8 @@ int cuda_err(cudaError_t e, const char* what) {
 }
 
 // ---- plans ------------------------------------------------------------------------------------
-enum PlanKind { P_AUTO = -1, P_NARROW = 0, P_VEC16 = 1, P_VEC16X = 2, P_REALIGN = 3, P_REALIGNX = 4, P_BULK = 5 };
+enum PlanKind { P_AUTO = -1, P_NARROW = 0, P_VEC16 = 1, P_VEC16X = 2, P_REALIGN = 3, P_REALIGNX = 4, P_BULK = 5,
+                P_PAPER_NAIVE = 6, P_PAPER_SHIFT = 7 };
 
 struct Plan {
   PlanKind kind;
@@ -63,6 +64,8 @@ const char* plan_name(const Plan& p) {
                      case 8: return "realign.g8"; case 16: return "realign.g16"; default: return "realign.g32"; }
     case P_REALIGNX: return "realign.g32x";
     case P_BULK: return "bulk";
+    case P_PAPER_NAIVE: return "paper_naive";
+    case P_PAPER_SHIFT: return "paper_shift";
     default: return "invalid";
   }
 }
@@ -120,6 +123,11 @@ bool choose_plan(uint64_t base, uint64_t rows, uint64_t rb, uint64_t out, PlanKi
       if (!aligned || rb > (uint64_t)ut::kBulkMaxRow) return false;
       *p = Plan{k, 32, false};
       return true;
+    case P_PAPER_NAIVE:
+    case P_PAPER_SHIFT:
+      if (((base | rb | out) & 3) != 0) return false;
+      *p = Plan{k, 1, false};
+      return true;
     default:
       return false;
   }
@@ -134,6 +142,8 @@ PlanKind parse_plan(const char* s, bool* ok) {
   if (!strcmp(s, "realign")) return P_REALIGN;
   if (!strcmp(s, "realignx")) return P_REALIGNX;
   if (!strcmp(s, "bulk")) return P_BULK;
+  if (!strcmp(s, "paper_naive")) return P_PAPER_NAIVE;
+  if (!strcmp(s, "paper_shift")) return P_PAPER_SHIFT;
   *ok = false;
   return P_AUTO;
 }
@@ -334,6 +344,16 @@ cudaError_t launch_plan(const Plan& p, int sms, cudaStream_t st, const ut::Gathe
       auto k = ut::k_multi<kUx, false, false, PERM>;
       return launch(k, grid_for(k, sms, a.n, cap), st, a);
     }
+    case P_PAPER_NAIVE:
+    case P_PAPER_SHIFT: {
+      // the paper's kernels visit rows in index order; with a perm they would not be the paper's
+      if (PERM) return cudaErrorInvalidValue;
+      const uint64_t threads = a.n * (a.rb >> 2);
+      const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)sms * 8, (threads + 255) / 256));
+      if (p.kind == P_PAPER_NAIVE) ut::k_paper<false><<<grid, 256, 0, st>>>(a);
+      else ut::k_paper<true><<<grid, 256, 0, st>>>(a);
+      return cudaGetLastError();
+    }
     case P_BULK: {
       constexpr int U = 4;
       auto k = ut::k_bulk<U, PERM>;
@@ -387,7 +407,7 @@ int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n
   cudaError_t e;
   s->rows += n;
   s->bytes += n * t->rb;
-  if (!want_reorder(t, n)) {
+  if (!want_reorder(t, n) || p.kind == P_PAPER_NAIVE || p.kind == P_PAPER_SHIFT) {
     e = timed_launch<false>(t, s, p, st, a, host_out);
     if (e != cudaSuccess) return cuda_err(e, plan_name(p));
     return UT_OK;

@@ -432,6 +432,39 @@ __global__ void __launch_bounds__(256, 1) k_bulk(GatherArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// The paper's own indexing kernels, for the ablation only (never auto-selected):
+//   paper_naive — PyTorch's stock index kernel as PAPER.md:557-558 describes it: one thread per
+//                 4-B feature, rows contiguous in thread space (thread r*W + j copies element j
+//                 of row idx[r] to output element r*W + j).
+//   paper_shift — the circular shift of PAPER.md:562-566 (reading R13): thread j of row r copies
+//                 element (j + s_r) mod W with s_r = (r*W - idx[r]*W) mod 32, writing the same
+//                 rotated output position ("the output indices are also identically adjusted").
+// Both need rb % 4 == 0 and 4-B aligned base and out. W = rb / 4.
+template <bool SHIFT>
+__global__ void __launch_bounds__(256) k_paper(GatherArgs a) {
+  const uint64_t W = a.rb >> 2;
+  const uint64_t total = a.n * W;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+    const uint64_t r = t / W;
+    const uint64_t j = t - r * W;
+    const int64_t g = __ldg(a.idx + r);
+    const bool ok = (uint64_t)g < a.rows;
+    uint64_t e = j;
+    if (SHIFT) {
+      const uint64_t s = ((r * W) - ((uint64_t)(ok ? g : 0) * W)) & 31ull;   // mod L = 32
+      e = j + s;
+      if (e >= W) e -= W;      // "adding or subtracting the length of the node feature"
+      if (e >= W) e %= W;      // (only when W < 32)
+    }
+    uint32_t v = 0;
+    if (ok) v = __ldg(reinterpret_cast<const uint32_t*>(a.tbase) + (uint64_t)g * W + e);
+    reinterpret_cast<uint32_t*>(a.out)[r * W + e] = v;
+    if (!ok && j == 0) record_bad(a.err, r);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // Translation-locality reorder: a counting sort of the work items by the table
 // region (1 << shift bytes, at most kMaxBuckets regions) their row starts in. The visiting order
 // changes, the result does not: every work item still writes its own output row.
