@@ -276,9 +276,10 @@ cudaError_t launch(K kernel, int grid, cudaStream_t st, const ut::GatherArgs& a)
 
 // Launch shape. "dense": every SM full of warps, U row-steps in flight per warp — right while the
 // table fits the translation reach. "sparse" (reordered gathers from tables beyond the reach):
-// one row-step per warp on a quarter of the SMs (~300 rows, ~150-300 KB in flight — enough for
-// the link's bandwidth x loaded latency of ~3.7 us), because more rows in flight touch more
-// translation pages at once and lose more than they hide (measured sweep).
+// one row-step per warp on 3/8 of the SMs (~440 rows, ~220 KB in flight — enough for the link's
+// bandwidth x loaded latency of ~3.7 us), because more rows in flight touch more translation
+// pages at once and lose more than they hide (measured sweep: 37 blocks 40.8,
+// 55 blocks 43.1, 74 blocks 42.0, 110 blocks 36.9 GB/s on the papers shape).
 struct Shape {
   bool sparse;
   int cap_blocks;
@@ -495,7 +496,7 @@ Shape shape_for(const ut_table* t, const DevState* s, bool reordered, uint64_t n
   // stores into mapped host memory add their own latency to every row: keep the dense shape there
   bool sparse = t->conc == 1 ||
                 (t->conc == -1 && reordered && !host_out && t->bytes > (1ull << 30) && thin);
-  int cap = env_blocks > 0 ? env_blocks : std::max(1, s->sms / 4);
+  int cap = env_blocks > 0 ? env_blocks : std::max(1, s->sms * 3 / 8);   // 55 of 148 SMs
   return Shape{sparse, cap};
 }
 
