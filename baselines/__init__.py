@@ -32,3 +32,17 @@ def cpu_staged_gather(table_addr: int, rb: int, idx_addr: int, n: int, staging_a
         _lib.cpu_staged_gather.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
                                            ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int]
     _lib.cpu_staged_gather(table_addr, rb, idx_addr, n, staging_addr, threads)
+
+
+def host_read_gbs(addr: int, nbytes: int, threads: int = 0, reps: int = 3) -> float:
+    """Best-of-`reps` multithreaded host read bandwidth over [addr, addr+nbytes) (GB/s)."""
+    import time
+    L = ctypes.CDLL(build())
+    L.host_read_sum.restype = ctypes.c_uint64
+    L.host_read_sum.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int]
+    best = 0.0
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        L.host_read_sum(addr, nbytes, threads)
+        best = max(best, nbytes / (time.perf_counter() - t0) / 1e9)
+    return best

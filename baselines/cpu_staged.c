@@ -19,3 +19,17 @@ void cpu_staged_gather(const uint8_t* table, uint64_t rb, const int64_t* idx, ui
     for (int64_t i = 0; i < (int64_t)n; ++i)
         memcpy(staging + (uint64_t)i * rb, table + (uint64_t)idx[i] * rb, rb);
 }
+
+/* Host DRAM read bandwidth probe for the per-box roofline (min(R_concurrent, R_dram), SURVEY
+ * §8d): all threads stream-read [p, p+bytes) with 64-bit loads; returns a checksum so the reads
+ * are not elided. */
+uint64_t host_read_sum(const uint8_t* p, uint64_t bytes, int threads)
+{
+    int nt = threads > 0 ? threads : omp_get_max_threads();
+    const uint64_t* q = (const uint64_t*)p;
+    int64_t words = (int64_t)(bytes / 8);
+    uint64_t acc = 0;
+#pragma omp parallel for schedule(static) num_threads(nt) reduction(^:acc)
+    for (int64_t i = 0; i < words; ++i) acc ^= q[i];
+    return acc;
+}

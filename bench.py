@@ -278,6 +278,23 @@ def run_reference(args, spec, dist):
     hb.close()
 
 
+def traffic_model(spec: dict, lists) -> dict:
+    """Honest-bytes accounting per step: unique-row bytes, and the link bytes and
+    requests a line-aligned warp kernel cannot go below — the 32-B sectors and 128-B lines the
+    rows touch (the table starts page-aligned in bench)."""
+    rb = spec["row_bytes"]
+    uniq, sect, lines = [], [], []
+    for l in lists:
+        start = l.astype(np.int64) * rb
+        uniq.append(np.unique(l).size * rb)
+        sect.append(int(((start + rb - 1) // 32 - start // 32 + 1).sum()) * 32)
+        lines.append(int(((start + rb - 1) // 128 - start // 128 + 1).sum()))
+    m = lambda v: float(np.mean(v)) if v else 0.0
+    return {"unique_row_mb_per_step": round(m(uniq) / 1e6, 2),
+            "sector_floor_mb_per_step": round(m(sect) / 1e6, 2),
+            "line_requests_per_step": round(m(lines), 1)}
+
+
 def config_block(spec: dict, lists, world: int) -> dict:
     rows_per_step = float(np.mean([l.size for l in lists])) if lists else 0.0
     c = {"workload": spec["workload"], "table_rows": spec["rows"], "row_bytes": spec["row_bytes"],
@@ -286,6 +303,7 @@ def config_block(spec: dict, lists, world: int) -> dict:
          "mb_per_step_per_gpu": round(rows_per_step * spec["row_bytes"] / 1e6, 2),
          "parallelism": f"dp{world} (independent minibatches per GPU, one shared host table)",
          "l2": "flushed (256 MiB write) between timed steps, outside the per-step events"}
+    c.update(traffic_model(spec, lists[:8]))
     if spec["kind"] == "graphsage":
         c.update({"batch": spec["batch"], "fanouts": spec["fanouts"], "graph_edges": spec["edges"]})
     else:
@@ -406,6 +424,22 @@ def run_ut(args, spec, dist):
                "path": "ut_gather_host: idx H2D copy, then the gather kernel stores rows into pinned host memory"}
         del out_host, idx_host
 
+    # optional NCCL all-reduce smoke step (SURVEY §2.3 ii): off the gather path, untimed
+    ar = None
+    if args.allreduce_smoke and world > 1:
+        g = torch.full((1 << 20,), float(rank + 1), dtype=torch.float32, device="cuda")
+        t1 = time.perf_counter()
+        dist.pg.all_reduce(g)
+        torch.cuda.synchronize()
+        ar = {"ok": bool((g == world * (world + 1) / 2).all().item()), "bytes": g.numel() * 4,
+              "ms": round((time.perf_counter() - t1) * 1e3, 3), "backend": dist.pg.get_backend()}
+
+    # per-box roofline term: host DRAM read bandwidth over the table (all host cores, rank 0)
+    dram = None
+    if rank == 0 and not args.no_cpu:
+        import baselines
+        dram = round(baselines.host_read_gbs(hb.addr, min(spec["rows"] * spec["row_bytes"], 8 << 30)), 2)
+
     # context baselines on rank 0 at N=1: the oracle and the paper's CPU-centric path
     cpu_base, py_base = None, None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -426,6 +460,8 @@ def run_ut(args, spec, dist):
             "per_gpu_gbs": round(per_gpu, 3),
             "h2d_memcpy_gbs": round(link, 3),
             "h2d_memcpy_concurrent_gbs": round(link_sum, 3),
+            "host_dram_read_gbs": dram,
+            "box_roofline_gbs": round(min(link_sum, dram), 3) if dram else round(link_sum, 3),
             "frac_of_link": round(per_gpu / link, 4),
             "plan": table.plan,
             "roofline": {"bound": "pcie_h2d", "achieved": round(achieved, 3),
@@ -436,7 +472,7 @@ def run_ut(args, spec, dist):
             "cpu_baseline": cpu_base, "py_baseline": py_base, "e2e": e2e,
             "gpu_launches": n_launch, "clocks": clk,
             "ranks_per_gpu": max(1, world // max(1, torch.cuda.device_count())),
-            "parity_checked": parity, "register_s": round(reg_s, 3),
+            "parity_checked": parity, "register_s": round(reg_s, 3), "allreduce_smoke": ar,
             "wall_ms_per_step": round(max_wall / args.steps * 1e3, 3),
         }
         print(json.dumps(line), flush=True)
@@ -490,6 +526,8 @@ def main(argv=None):
     ap.add_argument("--no-check", dest="check", action="store_false")
     ap.add_argument("--backend", default="nccl", help="process-group backend at N > 1")
     ap.add_argument("--presort", action="store_true", help="experiment: sort index lists on the host")
+    ap.add_argument("--allreduce-smoke", action="store_true",
+                    help="N > 1: one untimed NCCL all-reduce of a 4-MB fp32 buffer after timing")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
