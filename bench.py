@@ -311,6 +311,16 @@ def config_block(spec: dict, lists, world: int) -> dict:
     return c
 
 
+class _Owned:
+    """Stand-in for HostBuffer when the table's memory belongs to the library (ut_create)."""
+
+    def __init__(self, addr):
+        self.addr = addr
+
+    def close(self, unlink=False):
+        pass
+
+
 def run_ut(args, spec, dist):
     import torch
 
@@ -328,9 +338,17 @@ def run_ut(args, spec, dist):
     import paper_2101_07956_b200 as ut
 
     tag = f"{spec['config'].replace(':', '_')}_{os.environ.get('MASTER_PORT', '0')}"
-    hb = open_table(spec, rank, world, seed, dist, tag)
     t_reg = time.perf_counter()
-    table = ut.Table(hb.addr, spec["rows"], spec["row_bytes"])
+    if args.alloc == "register":
+        hb = open_table(spec, rank, world, seed, dist, tag)
+        t_reg = time.perf_counter()
+        table = ut.Table(hb.addr, spec["rows"], spec["row_bytes"])
+    else:   # the paper's to("unified"): a library-owned table (N = 1 only)
+        assert world == 1, "--alloc other than 'register' is single-process"
+        table = ut.Table.create(spec["rows"], spec["row_bytes"], args.alloc)
+        workloads.fill_table(table.host_addr, spec["rows"], spec["row_bytes"], seed,
+                             threads=os.cpu_count() or 1)
+        hb = _Owned(table.host_addr)
     reg_s = time.perf_counter() - t_reg
     if args.plan:
         for p in args.plan.split(","):
@@ -463,7 +481,7 @@ def run_ut(args, spec, dist):
             "host_dram_read_gbs": dram,
             "box_roofline_gbs": round(min(link_sum, dram), 3) if dram else round(link_sum, 3),
             "frac_of_link": round(per_gpu / link, 4),
-            "plan": table.plan,
+            "plan": table.plan, "table_memory": args.alloc,
             "roofline": {"bound": "pcie_h2d", "achieved": round(achieved, 3),
                          "peak": round(link, 3), "unit": "GB/s",
                          "frac": round(achieved / link, 4), "traffic": None,
@@ -526,6 +544,8 @@ def main(argv=None):
     ap.add_argument("--no-check", dest="check", action="store_false")
     ap.add_argument("--backend", default="nccl", help="process-group backend at N > 1")
     ap.add_argument("--presort", action="store_true", help="experiment: sort index lists on the host")
+    ap.add_argument("--alloc", default="register", choices=["register", "pinned", "managed", "vmm"],
+                    help="table memory: caller mmap + ut_register (default) or ut_create(kind)")
     ap.add_argument("--allreduce-smoke", action="store_true",
                     help="N > 1: one untimed NCCL all-reduce of a 4-MB fp32 buffer after timing")
     args = ap.parse_args(argv)

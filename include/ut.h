@@ -82,6 +82,30 @@ typedef enum ut_status {
 UT_API ut_table* ut_register(const void* host_ptr, uint64_t rows, uint64_t row_bytes);
 
 /*
+ * ut_create — the paper's own form, `t.to("unified")` (Table 1; §4.4
+ * P:530-531 "a new memory allocator ... for all unified tensors"): allocate a NEW host-resident
+ * table that the GPU maps, copy `src` into it (src may be NULL: the caller fills *host_out), and
+ * return its handle. Kinds (SURVEY NEXT-4 registration variants):
+ *   UT_ALLOC_PINNED    cudaHostAlloc(Portable|Mapped) page-locked host memory;
+ *   UT_ALLOC_MANAGED   cudaMallocManaged + cudaMemAdvise(SetPreferredLocation = CPU,
+ *                      SetAccessedBy = current device): the paper's default advice for unified
+ *                      tensors (Table 2) — data stays in host memory, GPU maps it;
+ *   UT_ALLOC_VMM_HOST  cuMemCreate(location HOST_NUMA of the current device) in 2-MiB granules,
+ *                      mapped read/write for the device and the host.
+ * *host_out receives the host (= device, UVA) address of the rows * row_bytes bytes; the memory
+ * is owned by the table and freed by ut_release. Returns NULL on failure (UT_EINVAL /
+ * UT_ENOMEM / UT_ECUDA / UT_ENOTSUP via ut_last_error).
+ */
+typedef enum ut_alloc_kind {
+  UT_ALLOC_PINNED = 0,
+  UT_ALLOC_MANAGED = 1,
+  UT_ALLOC_VMM_HOST = 2
+} ut_alloc_kind;
+
+UT_API ut_table* ut_create(const void* src, uint64_t rows, uint64_t row_bytes, int kind,
+                           void** host_out);
+
+/*
  * ut_gather — out_dev[i*rb .. (i+1)*rb) = row idx_dev[i] of the table, for i in [0, n).
  * The paper's `input_features = features[neighbor_id]` with a GPU index
  * tensor and a GPU output.
@@ -189,6 +213,7 @@ typedef struct ut_table_info {
   uint64_t host_addr;     /* host_ptr as an integer                                        */
   uint64_t dev_addr;      /* device address of host_ptr on the registering device          */
   int registered;         /* 1 if ut_register pinned the memory, 0 if it adopted it          */
+  int alloc_kind;         /* ut_alloc_kind for ut_create tables, -1 for caller memory       */
   int read_only;          /* 1 if registered with cudaHostRegisterReadOnly                   */
   int base_mod128;        /* host_ptr mod 128                                               */
   int device;             /* device that was current at registration                        */

@@ -28,7 +28,9 @@ UT_OK, UT_EINVAL, UT_ENOMEM, UT_ECUDA, UT_ERANGE, UT_ENOTSUP = 0, -1, -2, -3, -4
 # Every symbol include/ut.h declares (tests check the library exports exactly these).
 ABI = ("ut_register", "ut_gather", "ut_gather_host", "ut_release", "ut_error_pos",
        "ut_last_error", "ut_plan_name", "ut_plan_probe", "ut_set_plan", "ut_table_get_info",
-       "ut_get_stats")
+       "ut_get_stats", "ut_create")
+
+UT_ALLOC = {"pinned": 0, "managed": 1, "vmm": 2}
 
 
 class UTError(RuntimeError):
@@ -40,7 +42,8 @@ class UTError(RuntimeError):
 class _Info(ctypes.Structure):
     _fields_ = [("rows", ctypes.c_uint64), ("row_bytes", ctypes.c_uint64),
                 ("host_addr", ctypes.c_uint64), ("dev_addr", ctypes.c_uint64),
-                ("registered", ctypes.c_int), ("read_only", ctypes.c_int),
+                ("registered", ctypes.c_int), ("alloc_kind", ctypes.c_int),
+                ("read_only", ctypes.c_int),
                 ("base_mod128", ctypes.c_int), ("device", ctypes.c_int)]
 
 
@@ -74,6 +77,8 @@ def _load():
     L.ut_set_plan.argtypes = [vp, ctypes.c_char_p]
     L.ut_table_get_info.restype = ctypes.c_int
     L.ut_table_get_info.argtypes = [vp, ctypes.POINTER(_Info)]
+    L.ut_create.restype = vp
+    L.ut_create.argtypes = [vp, u64, u64, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]
     L.ut_get_stats.restype = ctypes.c_int
     L.ut_get_stats.argtypes = [vp, ctypes.POINTER(_Stats), ctypes.c_int]
     return L
@@ -103,6 +108,16 @@ def ut_register(host_addr: int, rows: int, row_bytes: int) -> int:
         code, msg = last_error()
         raise UTError(code, msg)
     return h
+
+
+def ut_create(src: int, rows: int, row_bytes: int, kind: int) -> tuple[int, int]:
+    """(handle, host address) of a new library-owned table (src 0/None: left for the caller)."""
+    host = ctypes.c_void_p()
+    h = _lib.ut_create(src or None, rows, row_bytes, kind, ctypes.byref(host))
+    if not h:
+        code, msg = last_error()
+        raise UTError(code, msg)
+    return h, int(host.value)
 
 
 def ut_gather(t: int, idx_dev: int, n: int, out_dev: int, stream: int = 0) -> None:
@@ -186,6 +201,25 @@ class Table:
                 row_bytes = nbytes // rows
         self.rows, self.row_bytes, self.host_addr = int(rows), int(row_bytes), int(addr)
         self.handle = ut_register(self.host_addr, self.rows, self.row_bytes)
+
+    @classmethod
+    def create(cls, rows: int, row_bytes: int, kind: str = "pinned", src=None) -> "Table":
+        """The paper's `to("unified")`: a new host-resident table of `kind` ("pinned",
+        "managed" or "vmm") owned by the library; fill it through `.array()` or copy `src`."""
+        addr = None
+        if src is not None:
+            addr = src.ctypes.data if hasattr(src, "ctypes") else src.data_ptr()
+        self = cls.__new__(cls)
+        self._keep = src
+        self.handle, self.host_addr = ut_create(addr, rows, row_bytes, UT_ALLOC[kind])
+        self.rows, self.row_bytes = int(rows), int(row_bytes)
+        return self
+
+    def array(self):
+        """uint8 numpy view of the table's host bytes (no copy)."""
+        import numpy as np
+        buf = (ctypes.c_uint8 * (self.rows * self.row_bytes)).from_address(self.host_addr)
+        return np.ctypeslib.as_array(buf)
 
     @property
     def plan(self) -> str:

@@ -5,6 +5,7 @@
 // and mapped in place (cudaHostRegister Portable|Mapped[|ReadOnly]) instead of copied into a new
 // allocation (reading R1), and `unified_tensor[gpu_tensor]`
 // is ut_gather. The kernels are in ut_kernels.cuh.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -180,6 +181,10 @@ struct ut_table {
   const uint8_t* reg_base = nullptr;   // page-aligned registered range
   uint64_t reg_len = 0;
   int registered = 0, read_only = 0, device = 0;
+  int alloc_kind = -1;                  // ut_create: ut_alloc_kind; -1 = caller memory
+  bool direct_va = false;               // device address == host address (managed / VMM)
+  unsigned long long vmm_handle = 0;    // CUmemGenericAllocationHandle
+  uint64_t vmm_bytes = 0;
   PlanKind forced = P_AUTO;
   int reorder = -1;                     // -1 auto, 0 off, 1 on (ut_set_plan "reorder=...")
   bool timing = false;                  // ut_set_plan "timing=on"
@@ -204,9 +209,11 @@ int dev_state(const ut_table* ct, DevState** out) {
   }
   std::lock_guard<std::mutex> lk(t->mu);
   if (!s->init) {
-    void* dp = nullptr;
-    e = cudaHostGetDevicePointer(&dp, const_cast<uint8_t*>(t->reg_base), 0);
-    if (e != cudaSuccess) return cuda_err(e, "cudaHostGetDevicePointer");
+    void* dp = const_cast<uint8_t*>(t->reg_base);
+    if (!t->direct_va) {
+      e = cudaHostGetDevicePointer(&dp, const_cast<uint8_t*>(t->reg_base), 0);
+      if (e != cudaSuccess) return cuda_err(e, "cudaHostGetDevicePointer");
+    }
     unsigned long long* err = nullptr;
     e = cudaMalloc(&err, sizeof *err);
     if (e != cudaSuccess) return cuda_err(e, "cudaMalloc(error word)");
@@ -495,7 +502,8 @@ Shape shape_for(const ut_table* t, const DevState* s, bool reordered, uint64_t n
   const bool thin = n * t->rb < (32ull << 10) * regions;
   // stores into mapped host memory add their own latency to every row: keep the dense shape there
   bool sparse = t->conc == 1 ||
-                (t->conc == -1 && reordered && !host_out && t->bytes > (1ull << 30) && thin);
+                (t->conc == -1 && reordered && !host_out && t->bytes > (1ull << 30) && thin &&
+                 t->alloc_kind != UT_ALLOC_MANAGED);
   int cap = env_blocks > 0 ? env_blocks : std::max(1, s->sms * 3 / 8);   // 55 of 148 SMs
   return Shape{sparse, cap};
 }
@@ -504,9 +512,13 @@ bool want_reorder(const ut_table* t, uint64_t n) {
   if (t->reorder == 0) return false;
   if (t->reorder == 1) return true;
   if (n < 4096 || n * t->rb < (4ull << 20)) return false;
-  // beyond the ~1-GiB translation reach every row size gains; below it only small rows, whose
-  // request rate (not bytes) is the limit, gain from visiting neighbouring rows together
-  return t->bytes > (1ull << 30) || (t->rb <= 128 && t->bytes > (64ull << 20));
+  // beyond the ~1-GiB translation reach of registered / pinned memory every row size gains;
+  // below it — and on managed tables, whose mappings have no such reach limit on this box —
+  // only small rows, whose request rate (not bytes) is the limit, gain from visiting
+  // neighbouring rows together
+  const bool small_rows = t->rb <= 128 && t->bytes > (64ull << 20);
+  if (t->alloc_kind == UT_ALLOC_MANAGED) return small_rows;
+  return t->bytes > (1ull << 30) || small_rows;
 }
 
 }  // namespace
@@ -590,6 +602,171 @@ ut_table* ut_register(const void* host_ptr, uint64_t rows, uint64_t row_bytes) {
     set_err(code, "%s", msg);
     return nullptr;
   }
+  g_err_code = UT_OK;
+  g_err_msg[0] = 0;
+  return t;
+}
+
+}  // extern "C"
+
+namespace {
+
+template <typename F>
+F driver_fn(const char* name) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<F>(fn);
+}
+
+// cuMemCreate(HOST_NUMA) + reserve + map + access for the device and the host.
+int vmm_host_alloc(int dev, uint64_t bytes, void** va_out, uint64_t* size_out,
+                   unsigned long long* handle_out) {
+  using PGran = CUresult (*)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags);
+  using PCreate = CUresult (*)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*,
+                               unsigned long long);
+  using PReserve = CUresult (*)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+  using PMap = CUresult (*)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+  using PAccess = CUresult (*)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+  using PRelease = CUresult (*)(CUmemGenericAllocationHandle);
+  using PFree = CUresult (*)(CUdeviceptr, size_t);
+  auto gran_f = driver_fn<PGran>("cuMemGetAllocationGranularity");
+  auto create_f = driver_fn<PCreate>("cuMemCreate");
+  auto reserve_f = driver_fn<PReserve>("cuMemAddressReserve");
+  auto map_f = driver_fn<PMap>("cuMemMap");
+  auto access_f = driver_fn<PAccess>("cuMemSetAccess");
+  auto release_f = driver_fn<PRelease>("cuMemRelease");
+  auto free_f = driver_fn<PFree>("cuMemAddressFree");
+  if (!gran_f || !create_f || !reserve_f || !map_f || !access_f || !release_f || !free_f)
+    return set_err(UT_ENOTSUP, "driver VMM entry points unavailable");
+  int numa = 0;
+  cudaDeviceGetAttribute(&numa, cudaDevAttrHostNumaId, dev);
+  CUmemAllocationProp prop{};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_HOST_NUMA;
+  prop.location.id = numa < 0 ? 0 : numa;
+  size_t gran = 0;
+  if (gran_f(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || !gran)
+    return set_err(UT_ENOTSUP, "cuMemGetAllocationGranularity(HOST_NUMA) failed");
+  const uint64_t size = (bytes + gran - 1) / gran * gran;
+  CUmemGenericAllocationHandle h = 0;
+  if (create_f(&h, size, &prop, 0) != CUDA_SUCCESS)
+    return set_err(UT_ENOMEM, "cuMemCreate(HOST_NUMA, %llu bytes) failed", (unsigned long long)size);
+  CUdeviceptr va = 0;
+  if (reserve_f(&va, size, gran, 0, 0) != CUDA_SUCCESS) {
+    release_f(h);
+    return set_err(UT_ENOMEM, "cuMemAddressReserve failed");
+  }
+  CUmemAccessDesc acc[2]{};
+  acc[0].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc[0].location.id = dev;
+  acc[0].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  acc[1].location = prop.location;
+  acc[1].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  if (map_f(va, size, 0, h, 0) != CUDA_SUCCESS || access_f(va, size, acc, 2) != CUDA_SUCCESS) {
+    free_f(va, size);
+    release_f(h);
+    return set_err(UT_ECUDA, "cuMemMap/cuMemSetAccess failed");
+  }
+  *va_out = (void*)va;
+  *size_out = size;
+  *handle_out = (unsigned long long)h;
+  return UT_OK;
+}
+
+void vmm_host_free(void* va, uint64_t size, unsigned long long handle) {
+  using PUnmap = CUresult (*)(CUdeviceptr, size_t);
+  using PRelease = CUresult (*)(CUmemGenericAllocationHandle);
+  using PFree = CUresult (*)(CUdeviceptr, size_t);
+  auto unmap_f = driver_fn<PUnmap>("cuMemUnmap");
+  auto release_f = driver_fn<PRelease>("cuMemRelease");
+  auto free_f = driver_fn<PFree>("cuMemAddressFree");
+  if (unmap_f) unmap_f((CUdeviceptr)va, size);
+  if (release_f) release_f((CUmemGenericAllocationHandle)handle);
+  if (free_f) free_f((CUdeviceptr)va, size);
+}
+
+}  // namespace
+
+extern "C" {
+
+ut_table* ut_create(const void* src, uint64_t rows, uint64_t row_bytes, int kind, void** host_out) {
+  if (!host_out) return set_err(UT_EINVAL, "host_out is NULL"), nullptr;
+  if (rows == 0 || row_bytes == 0) return set_err(UT_EINVAL, "rows and row_bytes must be >= 1"), nullptr;
+  if (rows > UINT64_MAX / row_bytes) return set_err(UT_EINVAL, "rows*row_bytes overflows"), nullptr;
+  const uint64_t bytes = rows * row_bytes;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_err(e, "cudaGetDevice"), nullptr;
+  void* p = nullptr;
+  uint64_t vmm_size = 0;
+  unsigned long long vmm_h = 0;
+  switch (kind) {
+    case UT_ALLOC_PINNED:
+      if ((e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable | cudaHostAllocMapped)) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(UT_ENOMEM, "cudaHostAlloc(%llu): %s", (unsigned long long)bytes,
+                       cudaGetErrorString(e)), nullptr;
+      }
+      break;
+    case UT_ALLOC_MANAGED: {
+      int managed = 0;
+      cudaDeviceGetAttribute(&managed, cudaDevAttrManagedMemory, dev);
+      if (!managed) return set_err(UT_ENOTSUP, "device %d has no managed memory", dev), nullptr;
+      if ((e = cudaMallocManaged(&p, bytes, cudaMemAttachGlobal)) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(UT_ENOMEM, "cudaMallocManaged(%llu): %s", (unsigned long long)bytes,
+                       cudaGetErrorString(e)), nullptr;
+      }
+      cudaMemLocation cpu{};
+      cpu.type = cudaMemLocationTypeHost;
+      cpu.id = 0;
+      cudaMemLocation gpu{};
+      gpu.type = cudaMemLocationTypeDevice;
+      gpu.id = dev;
+      if ((e = cudaMemAdvise(p, bytes, cudaMemAdviseSetPreferredLocation, cpu)) != cudaSuccess ||
+          (e = cudaMemAdvise(p, bytes, cudaMemAdviseSetAccessedBy, gpu)) != cudaSuccess) {
+        cudaFree(p);
+        return cuda_err(e, "cudaMemAdvise"), nullptr;
+      }
+      break;
+    }
+    case UT_ALLOC_VMM_HOST:
+      if (vmm_host_alloc(dev, bytes, &p, &vmm_size, &vmm_h) != UT_OK) return nullptr;
+      break;
+    default:
+      return set_err(UT_EINVAL, "unknown allocation kind %d", kind), nullptr;
+  }
+  if (src) memcpy(p, src, bytes);
+  ut_table* t = new (std::nothrow) ut_table;
+  if (!t) {
+    if (kind == UT_ALLOC_PINNED) cudaFreeHost(p);
+    else if (kind == UT_ALLOC_MANAGED) cudaFree(p);
+    else vmm_host_free(p, vmm_size, vmm_h);
+    return set_err(UT_ENOMEM, "out of host memory"), nullptr;
+  }
+  t->host = (const uint8_t*)p;
+  t->rows = rows;
+  t->rb = row_bytes;
+  t->bytes = bytes;
+  t->device = dev;
+  t->reg_base = (const uint8_t*)p;
+  t->reg_len = bytes;
+  t->alloc_kind = kind;
+  t->direct_va = kind != UT_ALLOC_PINNED;
+  t->vmm_handle = vmm_h;
+  t->vmm_bytes = vmm_size;
+  DevState* s;
+  if (dev_state(t, &s) != UT_OK) {
+    char msg[512];
+    int code = ut_last_error(msg, sizeof msg);
+    ut_release(t);
+    set_err(code, "%s", msg);
+    return nullptr;
+  }
+  *host_out = p;
   g_err_code = UT_OK;
   g_err_msg[0] = 0;
   return t;
@@ -738,6 +915,10 @@ int ut_release(ut_table* t) {
     cudaError_t e = cudaHostUnregister(const_cast<uint8_t*>(t->reg_base));
     if (e != cudaSuccess) rc = cuda_err(e, "cudaHostUnregister");
   }
+  if (t->alloc_kind == UT_ALLOC_PINNED) cudaFreeHost(const_cast<uint8_t*>(t->host));
+  else if (t->alloc_kind == UT_ALLOC_MANAGED) cudaFree(const_cast<uint8_t*>(t->host));
+  else if (t->alloc_kind == UT_ALLOC_VMM_HOST)
+    vmm_host_free(const_cast<uint8_t*>(t->host), t->vmm_bytes, t->vmm_handle);
   delete t;
   return rc;
 }
@@ -860,6 +1041,7 @@ int ut_table_get_info(const ut_table* t, ut_table_info* info) {
   const DevState& s = t->dev[t->device];
   info->dev_addr = s.init ? s.dev_base : 0;
   info->registered = t->registered;
+  info->alloc_kind = t->alloc_kind;
   info->read_only = t->read_only;
   info->base_mod128 = (int)((uint64_t)t->host & 127);
   info->device = t->device;

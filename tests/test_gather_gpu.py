@@ -226,3 +226,27 @@ def test_reorder_on_large_table(rb):
             _gather_check(t, hb.addr, rows, rb, idx, out_off=0)
             _gather_check(t, hb.addr, rows, rb, idx[: n // 3], out_off=4)
     hb.close()
+
+
+@pytest.mark.parametrize("kind", ["pinned", "managed", "vmm"])
+@pytest.mark.parametrize("rb", [68, 400, 4096])
+def test_create_library_owned_table(kind, rb):
+    """ut_create: the paper's to("unified") with each allocation kind; src copy and fill paths."""
+    rows = 20_000
+    src = np.empty(rows * rb, np.uint8)
+    workloads.fill_table(src, rows, rb, 31)
+    idx = workloads.uniform_idx(30_000, rows, 32)
+    idx[3] = rows - 1
+    want, _ = oracle.gather(src, rows, rb, idx)
+    with ut.Table.create(rows, rb, kind, src=src) as t:
+        info = t.info()
+        assert info["alloc_kind"] == ut.UT_ALLOC[kind] and info["registered"] == 0
+        assert t.array().tobytes() == src.tobytes()
+        for plan in ["auto", "reorder=on"]:
+            t.set_plan(plan)
+            out = t[torch.from_numpy(idx).cuda()]
+            assert out.cpu().numpy().tobytes() == want.tobytes()
+    with ut.Table.create(rows, rb, kind) as t:       # fill in place, no source copy
+        workloads.fill_table(t.host_addr, rows, rb, 31)
+        out = t[torch.from_numpy(idx).cuda()]
+        assert out.cpu().numpy().tobytes() == want.tobytes()
