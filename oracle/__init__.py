@@ -22,15 +22,18 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "ut_oracle.c")
+_SRC_SAMPLE = os.path.join(_HERE, "ut_oracle_sample.c")
 _SO = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 
 def build(force: bool = False) -> str:
     """Compile ut_oracle.c (plain C, -O2, single-threaded) into oracle/liboracle.so."""
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_SRC_SAMPLE))
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < newest:
         tmp = _SO + f".tmp{os.getpid()}"
-        subprocess.run(["gcc", "-O2", "-shared", "-fPIC", "-Wall", "-o", tmp, _SRC], check=True)
+        subprocess.run(["gcc", "-O2", "-shared", "-fPIC", "-Wall", "-o", tmp, _SRC, _SRC_SAMPLE],
+                       check=True)
         os.replace(tmp, _SO)
     return _SO
 
@@ -42,6 +45,13 @@ def _load():
         L.oracle_gather.restype = ctypes.c_int64
         L.oracle_gather.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
                                     ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]
+        L.oracle_sample.restype = ctypes.c_int64
+        L.oracle_sample.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                    ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int,
+                                    ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint64,
+                                    ctypes.POINTER(ctypes.c_uint64)]
+        L.oracle_sample_hash.restype = ctypes.c_uint64
+        L.oracle_sample_hash.argtypes = [ctypes.c_uint64] * 4
         _lib = L
     return _lib
 
@@ -70,3 +80,27 @@ def gather(table, rows: int, rb: int, idx) -> tuple[np.ndarray, int]:
         addr = int(table)
     bad = gather_into(addr, rows, rb, idx, out)
     return out, bad
+
+
+def sample(indptr_addr: int, indices_addr: int, n_nodes: int, seeds, fanouts, seed: int) -> np.ndarray:
+    """Oracle multi-hop neighbour sampling (ut_oracle_sample.c): the minibatch node list."""
+    seeds = np.ascontiguousarray(seeds, dtype=np.int64)
+    fan = np.ascontiguousarray(fanouts, dtype=np.int32)
+    need = ctypes.c_uint64(0)
+    cap = max(16, seeds.size * 4)
+    while True:
+        out = np.empty(cap, dtype=np.int64)
+        rc = _load().oracle_sample(indptr_addr, indices_addr, n_nodes, seeds.ctypes.data,
+                                   seeds.size, fan.ctypes.data, fan.size,
+                                   seed & 0xFFFFFFFFFFFFFFFF, out.ctypes.data, cap,
+                                   ctypes.byref(need))
+        if rc >= 0:
+            return out[:rc]
+        if rc == -1:
+            cap = int(need.value)
+            continue
+        raise ValueError("seed out of range" if rc == -2 else "allocation failure")
+
+
+def sample_hash(seed: int, hop: int, v: int, t: int) -> int:
+    return int(_load().oracle_sample_hash(seed & 0xFFFFFFFFFFFFFFFF, hop, v, t))

@@ -30,7 +30,7 @@ def build(force: bool = False) -> str:
     """Compile gen.c into workloads/libutgen.so (gcc, OpenMP)."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
         tmp = _SO + f".tmp{os.getpid()}"
-        subprocess.run(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-Wall", "-o", tmp, _SRC],
+        subprocess.run(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-Wall", "-o", tmp, _SRC, "-lm"],
                        check=True)
         os.replace(tmp, _SO)
     return _SO
@@ -48,6 +48,12 @@ def lib():
         L.gen_uniform_idx.restype = None
         L.gen_uniform_idx.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
                                       ctypes.c_uint64]
+        L.gen_chunglu_indptr.restype = ctypes.c_int64
+        L.gen_chunglu_indptr.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                                         ctypes.c_double, ctypes.c_uint64]
+        L.gen_chunglu_indices.restype = None
+        L.gen_chunglu_indices.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                          ctypes.c_double, ctypes.c_uint64, ctypes.c_int]
         L.gen_map.restype = ctypes.c_void_p
         L.gen_map.argtypes = [ctypes.c_uint64, ctypes.c_int]
         L.gen_unmap.restype = ctypes.c_int
@@ -173,3 +179,33 @@ class HostBuffer:
             self.close()
         except Exception:
             pass
+
+
+class CSRGraph:
+    """An explicit host CSR graph (indptr int64[N+1], indices int32[E]) in plain host memory:
+    the input of GPU-side neighbour sampling. Chung-Lu power law, see gen.c."""
+
+    def __init__(self, n_nodes: int, n_edges: int, seed: int = 1, gamma: float = 2.5,
+                 threads: int = 0):
+        self.n_nodes = int(n_nodes)
+        self._ip = HostBuffer((self.n_nodes + 1) * 8)
+        self.indptr = np.ctypeslib.as_array(
+            (ctypes.c_int64 * (self.n_nodes + 1)).from_address(self._ip.addr))
+        self.n_edges = int(lib().gen_chunglu_indptr(self._ip.addr, self.n_nodes, n_edges, gamma, seed))
+        self._ix = HostBuffer(max(1, self.n_edges) * 4)
+        self.indices = np.ctypeslib.as_array(
+            (ctypes.c_int32 * max(1, self.n_edges)).from_address(self._ix.addr))[: self.n_edges]
+        lib().gen_chunglu_indices(self._ip.addr, self._ix.addr, self.n_nodes, gamma, seed, threads)
+
+    @property
+    def indptr_addr(self) -> int:
+        return self._ip.addr
+
+    @property
+    def indices_addr(self) -> int:
+        return self._ix.addr
+
+    def close(self):
+        self.indptr = self.indices = None
+        self._ip.close()
+        self._ix.close()

@@ -99,3 +99,57 @@ void* gen_map_guarded(uint64_t bytes, void** map_base, uint64_t* map_len)
     *map_len = len;
     return p + pg + data - bytes;
 }
+
+/* ---- explicit CSR graph (for GPU-side sampling) ------------------------------
+ * Chung-Lu power law like workloads/graphsage.py, materialised: node of rank k is
+ * (k*A + B) mod N; deg(rank k) = max(1, round(E * (k+1)^-theta / W)); neighbour j of node v is
+ * the node of rank floor(F^-1(u)), u = U01(splitmix64(seed ^ (v*PHI + j))), F the continuous
+ * weight CDF. indptr is int64[N+1], indices int32[indptr[N]]. */
+#include <math.h>
+
+static uint64_t gcd_u64(uint64_t a, uint64_t b) { while (b) { uint64_t t = a % b; a = b; b = t; } return a; }
+
+static uint64_t coprime_mult(uint64_t n, uint64_t seed)
+{
+    uint64_t a = (splitmix64(seed) % n) | 1;
+    while (gcd_u64(a, n) != 1) a += 2;
+    return a % n;
+}
+
+/* Fills indptr[0..N] (int64). Returns the edge count indptr[N]. */
+int64_t gen_chunglu_indptr(int64_t* indptr, uint64_t N, uint64_t E, double gamma, uint64_t seed)
+{
+    const double theta = 1.0 / (gamma - 1.0), one = 1.0 - theta;
+    const double W = (pow((double)N + 0.5, one) - pow(0.5, one)) / one;
+    const uint64_t A = N > 1 ? coprime_mult(N, seed ^ 0x1234) : 0;
+    const uint64_t B = N > 1 ? splitmix64(seed ^ 0x5678) % N : 0;
+    for (uint64_t k = 0; k < N; ++k) {
+        double d = nearbyint((double)E * pow((double)k + 1.0, -theta) / W);
+        int64_t deg = d < 1.0 ? 1 : (int64_t)d;
+        uint64_t v = (uint64_t)(((__uint128_t)k * A + B) % N);
+        indptr[v + 1] = deg;
+    }
+    indptr[0] = 0;
+    for (uint64_t v = 0; v < N; ++v) indptr[v + 1] += indptr[v];
+    return indptr[N];
+}
+
+void gen_chunglu_indices(const int64_t* indptr, int32_t* indices, uint64_t N, double gamma,
+                         uint64_t seed, int threads)
+{
+    const double theta = 1.0 / (gamma - 1.0), one = 1.0 - theta;
+    const double cdf_hi = pow((double)N + 1.0, one) - 1.0;
+    const uint64_t A = N > 1 ? coprime_mult(N, seed ^ 0x1234) : 0;
+    const uint64_t B = N > 1 ? splitmix64(seed ^ 0x5678) % N : 0;
+    int nt = threads > 0 ? threads : omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 4096) num_threads(nt)
+    for (int64_t v = 0; v < (int64_t)N; ++v) {
+        for (int64_t p = indptr[v]; p < indptr[v + 1]; ++p) {
+            uint64_t h = splitmix64(splitmix64(seed ^ ((uint64_t)v * PHI + (uint64_t)(p - indptr[v]))));
+            double u = (double)(h >> 11) * (1.0 / 9007199254740992.0);
+            double x = pow(1.0 + u * cdf_hi, 1.0 / one) - 1.0;
+            uint64_t rank = x >= (double)(N - 1) ? N - 1 : (uint64_t)x;
+            indices[p] = (int32_t)(((__uint128_t)rank * A + B) % N);
+        }
+    }
+}
