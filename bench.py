@@ -355,6 +355,10 @@ def run_ut(args, spec, dist):
             table.set_plan(p)
     rb = spec["row_bytes"]
     stream = torch.cuda.current_stream()
+    sampler = None
+    if args.sample == "gpu":
+        sampler = GpuSampling(spec, rank, world, count, seed, ut, torch)
+        lists = sampler.node_lists_for_accounting()
     idx_dev = [torch.from_numpy(l).to("cuda") for l in lists]
     max_n = max(l.size for l in lists)
     out = torch.empty(max_n * rb, dtype=torch.uint8, device="cuda")
@@ -367,7 +371,11 @@ def run_ut(args, spec, dist):
 
     # parity (outside timing): the first minibatch against the oracle, byte for byte
     parity = None
-    if args.check:
+    if args.check and sampler is not None:
+        parity = sampler.check(hb.addr, table, out)
+        if not parity:
+            raise SystemExit(f"rank {rank}: parity failure (GPU sampling + gather)")
+    elif args.check:
         import oracle
         l = lists[0]
         want, bad = oracle.gather(hb.addr, spec["rows"], rb, l)
@@ -381,6 +389,9 @@ def run_ut(args, spec, dist):
     clocks.start()
     # warm-up
     for s in range(args.warmup):
+        if sampler is not None:
+            sampler.step(s, table, out)
+            continue
         l = idx_dev[s % count]
         table.gather(l, out=out[: l.numel() * rb])
     torch.cuda.synchronize()
@@ -393,15 +404,18 @@ def run_ut(args, spec, dist):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for s in range(args.steps):
-        l = idx_dev[(args.warmup + s) % count]
         flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        table.gather(l, out=out[: l.numel() * rb], stream=stream)
+        if sampler is not None:
+            nbytes += sampler.step(args.warmup + s, table, out) * rb
+        else:
+            l = idx_dev[(args.warmup + s) % count]
+            table.gather(l, out=out[: l.numel() * rb], stream=stream)
+            nbytes += l.numel() * rb
         e1.record(stream)
         evs.append((e0, e1))
-        nbytes += l.numel() * rb
     torch.cuda.synchronize()
     dist.barrier()
     wall = time.perf_counter() - t0
@@ -419,7 +433,7 @@ def run_ut(args, spec, dist):
 
     # end to end: host idx in (pinned), host rows out (pinned), through ut_gather_host
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and sampler is None:
         idx_host = [torch.from_numpy(x).pin_memory() for x in lists]
         out_host = torch.empty(max_n * rb, dtype=torch.uint8, pin_memory=True)
         for s in range(min(2, count)):
@@ -489,6 +503,7 @@ def run_ut(args, spec, dist):
                          "peak_source": "pinned cudaMemcpy H2D measured in this run (best of 10 x 1 GiB)"},
             "cpu_baseline": cpu_base, "py_baseline": py_base, "e2e": e2e,
             "gpu_launches": n_launch, "clocks": clk,
+            "sampling": sampler.report(args.steps) if sampler is not None else None,
             "ranks_per_gpu": max(1, world // max(1, torch.cuda.device_count())),
             "parity_checked": parity, "register_s": round(reg_s, 3), "allreduce_smoke": ar,
             "wall_ms_per_step": round(max_wall / args.steps * 1e3, 3),
@@ -500,6 +515,83 @@ def run_ut(args, spec, dist):
         hb.close(unlink=True)
     else:
         hb.close()
+
+
+class GpuSampling:
+    """`--sample gpu`: every step samples its minibatch on the GPU from a host-resident CSR graph
+    (ut_sample) and gathers the rows of the sampled nodes — the whole minibatch
+    preparation with no CPU in the loop. The CSR is an explicit Chung-Lu graph of the config's
+    N and E (workloads.CSRGraph); each step's 'batch' roots are the rank's slice of a seeded
+    permutation."""
+
+    def __init__(self, spec, rank, world, count, seed, ut, torch):
+        assert spec["kind"] == "graphsage", "--sample gpu needs a graphsage-shaped config"
+        self.torch, self.ut, self.spec = torch, ut, spec
+        self.csr = workloads.CSRGraph(spec["rows"], spec["edges"], seed=seed, threads=0)
+        self.graph = ut.Graph(self.csr.indptr_addr, self.csr.indices_addr, self.csr.n_nodes,
+                              self.csr.n_edges, keep=self.csr)
+        perm = np.random.default_rng(seed + 99).permutation(spec["rows"])
+        B = spec["batch"]
+        self.roots = [perm[((b * world + rank) * B) % spec["rows"]:][:B].astype(np.int64)
+                      for b in range(count)]
+        self.roots_dev = [torch.from_numpy(r).cuda() for r in self.roots]
+        self.fanouts = list(spec["fanouts"])
+        self.seed = seed
+        cap = B
+        for f in self.fanouts:
+            cap += cap * f
+        self.nodes = torch.empty(min(cap, spec["rows"]), dtype=torch.int64, device="cuda")
+        self.ms_sample, self.rows, self.mid = 0.0, 0, []
+
+    def node_lists_for_accounting(self):
+        """The minibatches' node lists, computed on the GPU once (for the traffic model and the
+        buffer sizes; the timed steps sample again)."""
+        out = []
+        for b, r in enumerate(self.roots_dev):
+            out.append(self.graph.sample(r, self.fanouts, self.seed + b, out=self.nodes).cpu().numpy())
+        return out
+
+    def step(self, s, table, out):
+        torch = self.torch
+        b = s % len(self.roots_dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        nodes = self.graph.sample(self.roots_dev[b], self.fanouts, self.seed + b, out=self.nodes)
+        e1.record()
+        self.mid.append((e0, e1))
+        n = nodes.numel()
+        table.gather(nodes, out=out[: n * self.spec["row_bytes"]])
+        self.rows += n
+        return n
+
+    def check(self, table_addr, table, out) -> bool:
+        import oracle
+        r = self.roots[0]
+        want_nodes = oracle.sample(self.csr.indptr_addr, self.csr.indices_addr, self.csr.n_nodes,
+                                   r, self.fanouts, self.seed)
+        got_nodes = self.graph.sample(self.roots_dev[0], self.fanouts, self.seed, out=self.nodes)
+        if not np.array_equal(got_nodes.cpu().numpy(), want_nodes):
+            return False
+        rb = self.spec["row_bytes"]
+        want, _ = oracle.gather(table_addr, self.spec["rows"], rb, want_nodes)
+        table.gather(got_nodes, out=out[: got_nodes.numel() * rb])
+        return out[: got_nodes.numel() * rb].cpu().numpy().tobytes() == want.tobytes()
+
+    def report(self, steps):
+        import time as _t
+        import oracle
+        self.torch.cuda.synchronize()
+        ms = [a.elapsed_time(b) for a, b in self.mid[-steps:]]
+        t0 = _t.perf_counter()
+        for b in range(3):
+            oracle.sample(self.csr.indptr_addr, self.csr.indices_addr, self.csr.n_nodes,
+                          self.roots[b], self.fanouts, self.seed + b)
+        cpu_ms = (_t.perf_counter() - t0) / 3 * 1e3
+        return {"where": "gpu (ut_sample over the host-resident CSR), inside every timed step",
+                "graph": f"explicit Chung-Lu CSR, N={self.csr.n_nodes}, E={self.csr.n_edges}",
+                "gpu_sample_ms_per_step": round(float(np.mean(ms)), 3),
+                "oracle_cpu_sample_ms_per_minibatch": round(cpu_ms, 2), "oracle_cores": 1}
 
 
 def cpu_staged_baseline(torch, table_addr, spec, lists, args):
@@ -546,6 +638,9 @@ def main(argv=None):
     ap.add_argument("--presort", action="store_true", help="experiment: sort index lists on the host")
     ap.add_argument("--alloc", default="register", choices=["register", "pinned", "managed", "vmm"],
                     help="table memory: caller mmap + ut_register (default) or ut_create(kind)")
+    ap.add_argument("--sample", default="cpu", choices=["cpu", "gpu"],
+                    help="cpu: index lists sampled before timing (default, the paper's split); "
+                         "gpu: ut_sample inside every timed step (SURVEY NEXT-2)")
     ap.add_argument("--allreduce-smoke", action="store_true",
                     help="N > 1: one untimed NCCL all-reduce of a 4-MB fp32 buffer after timing")
     args = ap.parse_args(argv)

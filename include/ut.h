@@ -76,7 +76,9 @@ typedef enum ut_status {
  *   rows       number of rows, >= 1.
  *   row_bytes  bytes per row, >= 1; rows * row_bytes must not overflow 64 bits.
  * The current CUDA device is used for registration; the mapping is Portable, so the handle
- * serves every device of the process. Returns NULL on failure (UT_EINVAL / UT_ENOMEM /
+ * serves every device of the process. Registration pins whole pages: the table should not share
+ * its first or last page with host buffers that other code hands to CUDA copies (allocate big
+ * tables page-aligned, e.g. mmap); pages already pinned by a neighbour are left to it. Returns NULL on failure (UT_EINVAL / UT_ENOMEM /
  * UT_ECUDA / UT_ENOTSUP via ut_last_error).
  */
 UT_API ut_table* ut_register(const void* host_ptr, uint64_t rows, uint64_t row_bytes);
@@ -188,6 +190,47 @@ UT_API const char* ut_plan_probe(uint64_t base, uint64_t rows, uint64_t row_byte
  * The environment variables UT_PLAN and UT_REORDER, read at ut_register, do the same.
  */
 UT_API int ut_set_plan(ut_table* t, const char* name);
+
+/* ---- GPU-side neighbour sampling over a host-resident CSR graph -------------
+ * The step before the gather that the paper leaves on the CPU. The CSR stays in
+ * host memory (pinned in place like a feature table) and GPU threads read it over the link. */
+typedef struct ut_graph ut_graph;
+
+/*
+ * ut_graph_register — pin a CSR graph in place for GPU sampling.
+ *   indptr   int64[n_nodes + 1], indptr[0] == 0, non-decreasing, indptr[n_nodes] == n_edges.
+ *   indices  int32[n_edges] neighbour ids in [0, n_nodes) (the caller guarantees the range).
+ *   n_nodes  in [1, 2^31).
+ * Both arrays are caller-owned and must stay valid and unmodified until ut_graph_release. The
+ * current device gets n_nodes bytes + 8*n_nodes bytes of sampler state. NULL on failure.
+ */
+UT_API ut_graph* ut_graph_register(const int64_t* indptr, const int32_t* indices, uint64_t n_nodes,
+                                   uint64_t n_edges);
+
+/* "indptr=hbm" keeps a device copy of indptr (8*(n_nodes+1) bytes) so only `indices` is read
+ * over the link; "indptr=host" (default) reads both over the link. */
+UT_API int ut_graph_set_option(ut_graph* g, const char* option);
+
+/*
+ * ut_sample — multi-hop neighbour sampling, reading R17 (= oracle/ut_oracle_sample.c):
+ * frontier_0 = seeds (first-appearance unique); at hop h each frontier node v takes
+ * min(deg(v), fanouts[h]) distinct neighbour slots (all when deg <= fanout, else one per stratum
+ * [floor(t*deg/f), floor((t+1)*deg/f)) chosen by the counter hash H(seed, h, v, t)); the next
+ * frontier is the old one followed by the not-yet-seen sampled neighbours in (v, t) order.
+ *   seeds_dev  n_seeds int64 node ids on the current device.
+ *   fanouts    n_hops host ints >= 0.
+ *   nodes_dev  device int64[cap]: receives the final frontier (the minibatch's node list, seeds
+ *              first) — the index list a following ut_gather reads.
+ *   *n_out     node count (set even when cap is too small, then UT_EINVAL is returned).
+ * Synchronises `stream` twice per hop to read sizes; the nodes are written stream-ordered.
+ * Returns UT_OK, UT_EINVAL, UT_ERANGE (a seed outside [0, n_nodes)), UT_ENOMEM or UT_ECUDA.
+ */
+UT_API int ut_sample(ut_graph* g, const int64_t* seeds_dev, uint64_t n_seeds, const int32_t* fanouts,
+                     int n_hops, uint64_t seed, int64_t* nodes_dev, uint64_t cap, uint64_t* n_out,
+                     ut_stream_t stream);
+
+/* Free the sampler state and unpin the CSR arrays (if ut_graph_register pinned them). */
+UT_API int ut_graph_release(ut_graph* g);
 
 /* Per-device counters of one table (for reports and the bench's launch count). */
 typedef struct ut_stats {

@@ -28,7 +28,8 @@ UT_OK, UT_EINVAL, UT_ENOMEM, UT_ECUDA, UT_ERANGE, UT_ENOTSUP = 0, -1, -2, -3, -4
 # Every symbol include/ut.h declares (tests check the library exports exactly these).
 ABI = ("ut_register", "ut_gather", "ut_gather_host", "ut_release", "ut_error_pos",
        "ut_last_error", "ut_plan_name", "ut_plan_probe", "ut_set_plan", "ut_table_get_info",
-       "ut_get_stats", "ut_create")
+       "ut_get_stats", "ut_create", "ut_graph_register", "ut_graph_set_option", "ut_sample",
+       "ut_graph_release")
 
 UT_ALLOC = {"pinned": 0, "managed": 1, "vmm": 2}
 
@@ -79,6 +80,15 @@ def _load():
     L.ut_table_get_info.argtypes = [vp, ctypes.POINTER(_Info)]
     L.ut_create.restype = vp
     L.ut_create.argtypes = [vp, u64, u64, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]
+    L.ut_graph_register.restype = vp
+    L.ut_graph_register.argtypes = [vp, vp, u64, u64]
+    L.ut_graph_set_option.restype = ctypes.c_int
+    L.ut_graph_set_option.argtypes = [vp, ctypes.c_char_p]
+    L.ut_sample.restype = ctypes.c_int
+    L.ut_sample.argtypes = [vp, vp, u64, vp, ctypes.c_int, u64, vp, u64,
+                            ctypes.POINTER(ctypes.c_uint64), vp]
+    L.ut_graph_release.restype = ctypes.c_int
+    L.ut_graph_release.argtypes = [vp]
     L.ut_get_stats.restype = ctypes.c_int
     L.ut_get_stats.argtypes = [vp, ctypes.POINTER(_Stats), ctypes.c_int]
     return L
@@ -162,6 +172,34 @@ def ut_get_stats(t: int, reset: bool = False) -> dict:
     st = _Stats()
     _check(_lib.ut_get_stats(t, ctypes.byref(st), 1 if reset else 0))
     return {k: getattr(st, k) for k, _ in _Stats._fields_}
+
+
+def ut_graph_register(indptr_addr: int, indices_addr: int, n_nodes: int, n_edges: int) -> int:
+    h = _lib.ut_graph_register(indptr_addr, indices_addr, n_nodes, n_edges)
+    if not h:
+        code, msg = last_error()
+        raise UTError(code, msg)
+    return h
+
+
+def ut_graph_set_option(g: int, option: str) -> None:
+    _check(_lib.ut_graph_set_option(g, option.encode()))
+
+
+def ut_sample(g: int, seeds_dev: int, n_seeds: int, fanouts, seed: int, nodes_dev: int, cap: int,
+              stream: int = 0) -> int:
+    fan = (ctypes.c_int32 * len(fanouts))(*fanouts)
+    n = ctypes.c_uint64(0)
+    rc = _lib.ut_sample(g, seeds_dev, n_seeds, fan, len(fanouts), seed & 0xFFFFFFFFFFFFFFFF,
+                        nodes_dev, cap, ctypes.byref(n), stream)
+    if rc != UT_OK:
+        code, msg = last_error()
+        raise UTError(rc, msg)
+    return int(n.value)
+
+
+def ut_graph_release(g: int) -> None:
+    _check(_lib.ut_graph_release(g))
 
 
 # ---- convenience ----------------------------------------------------------------------------
@@ -269,6 +307,49 @@ class Table:
     def close(self) -> None:
         if getattr(self, "handle", None):
             ut_release(self.handle)
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Graph:
+    """A host-resident CSR graph sampled by GPU threads."""
+
+    def __init__(self, indptr_addr: int, indices_addr: int, n_nodes: int, n_edges: int, keep=None):
+        self._keep = keep
+        self.n_nodes, self.n_edges = int(n_nodes), int(n_edges)
+        self.handle = ut_graph_register(indptr_addr, indices_addr, n_nodes, n_edges)
+
+    def set_option(self, option: str) -> None:
+        ut_graph_set_option(self.handle, option)
+
+    def sample(self, seeds, fanouts, seed: int, out=None, stream=None):
+        """Minibatch node list (CUDA int64 tensor, seeds first) for CUDA int64 `seeds`."""
+        import torch
+        assert seeds.is_cuda and seeds.dtype == torch.int64 and seeds.is_contiguous()
+        cap = seeds.numel()
+        for f in fanouts:
+            cap += cap * int(f)
+        cap = min(cap, self.n_nodes)
+        if out is None or out.numel() < cap:
+            out = torch.empty(max(1, cap), dtype=torch.int64, device=seeds.device)
+        n = ut_sample(self.handle, seeds.data_ptr(), seeds.numel(), list(fanouts), seed,
+                      out.data_ptr(), out.numel(), _stream_handle(stream))
+        return out[:n]
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            ut_graph_release(self.handle)
             self.handle = None
 
     def __enter__(self):

@@ -19,11 +19,10 @@
 #include <unistd.h>
 
 #include "ut.h"
+#include "ut_internal.h"
 #include "ut_kernels.cuh"
 
-namespace {
-
-constexpr int kMaxDev = 64;
+namespace utx {
 
 thread_local int g_err_code = UT_OK;
 thread_local char g_err_msg[512] = "";
@@ -40,6 +39,93 @@ int set_err(int code, const char* fmt, ...) {
 int cuda_err(cudaError_t e, const char* what) {
   return set_err(UT_ECUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
 }
+
+int pin_host(const void* p, uint64_t bytes, bool read_only, Pin* out) {
+  *out = Pin{};
+  cudaPointerAttributes attr{}, attr_end{};
+  cudaError_t e = cudaPointerGetAttributes(&attr, p);
+  cudaError_t e2 = cudaPointerGetAttributes(&attr_end, (const uint8_t*)p + bytes - 1);
+  if (e == cudaSuccess && e2 == cudaSuccess && attr.type == cudaMemoryTypeHost &&
+      attr_end.type == cudaMemoryTypeHost && attr.devicePointer != nullptr) {
+    out->base = (const uint8_t*)p;
+    out->len = bytes;
+    return UT_OK;
+  }
+  cudaGetLastError();
+  int dev = 0, ro_ok = 0;
+  cudaGetDevice(&dev);
+  if (read_only) cudaDeviceGetAttribute(&ro_ok, cudaDevAttrHostRegisterReadOnlySupported, dev);
+  const uint64_t pg = (uint64_t)sysconf(_SC_PAGESIZE);
+  const uint64_t lo = (uint64_t)p / pg * pg;
+  const uint64_t hi = ((uint64_t)p + bytes + pg - 1) / pg * pg;
+  unsigned flags = cudaHostRegisterPortable | cudaHostRegisterMapped;
+  e = cudaErrorUnknown;
+  if (ro_ok) {
+    e = cudaHostRegister((void*)lo, hi - lo, flags | cudaHostRegisterReadOnly);
+    if (e == cudaSuccess) out->read_only = 1;
+    else cudaGetLastError();
+  }
+  if (e != cudaSuccess) e = cudaHostRegister((void*)lo, hi - lo, flags);
+  uint64_t rlo = lo, rhi = hi;
+  if (e == cudaErrorHostMemoryAlreadyRegistered) {
+    // a neighbouring allocation registered the first and/or last page: pin the rest
+    cudaGetLastError();
+    auto pinned = [](uint64_t a) {
+      cudaPointerAttributes at{};
+      bool ok = cudaPointerGetAttributes(&at, (const void*)a) == cudaSuccess &&
+                at.type == cudaMemoryTypeHost;
+      cudaGetLastError();
+      return ok;
+    };
+    if (pinned(rlo)) rlo += pg;
+    if (rhi > rlo && pinned(rhi - 1)) rhi -= pg;
+    if (rlo >= rhi) {
+      out->base = (const uint8_t*)p;   // every page is already pinned by someone else
+      out->len = bytes;
+      return UT_OK;
+    }
+    e = cudaHostRegister((void*)rlo, rhi - rlo, flags);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    if (e == cudaErrorMemoryAllocation)
+      return set_err(UT_ENOMEM, "cudaHostRegister(%llu bytes): %s", (unsigned long long)(hi - lo),
+                     cudaGetErrorString(e));
+    return cuda_err(e, "cudaHostRegister");
+  }
+  out->base = (const uint8_t*)rlo;
+  out->len = rhi - rlo;
+  out->registered = 1;
+  return UT_OK;
+}
+
+void unpin_host(Pin* pin) {
+  if (pin->registered) cudaHostUnregister(const_cast<uint8_t*>(pin->base));
+  *pin = Pin{};
+}
+
+int pin_device_ptr(const Pin& pin, const void* p, uint64_t* dev) {
+  int d = 0, same = 0;
+  cudaGetDevice(&d);
+  cudaDeviceGetAttribute(&same, cudaDevAttrCanUseHostPointerForRegisteredMem, d);
+  if (same) {   // UVA: the host address is the device address of registered memory
+    *dev = (uint64_t)p;
+    return UT_OK;
+  }
+  void* dp = nullptr;
+  cudaError_t e = cudaHostGetDevicePointer(&dp, const_cast<uint8_t*>(pin.base), 0);
+  if (e != cudaSuccess) return cuda_err(e, "cudaHostGetDevicePointer");
+  *dev = (uint64_t)dp + ((uint64_t)p - (uint64_t)pin.base);
+  return UT_OK;
+}
+
+}  // namespace utx
+
+using namespace utx;
+
+namespace {
+
+constexpr int kMaxDev = 64;
 
 // ---- plans ------------------------------------------------------------------------------------
 enum PlanKind { P_AUTO = -1, P_NARROW = 0, P_VEC16 = 1, P_VEC16X = 2, P_REALIGN = 3, P_REALIGNX = 4, P_BULK = 5,
@@ -209,10 +295,12 @@ int dev_state(const ut_table* ct, DevState** out) {
   }
   std::lock_guard<std::mutex> lk(t->mu);
   if (!s->init) {
-    void* dp = const_cast<uint8_t*>(t->reg_base);
+    uint64_t dev_base = (uint64_t)t->host;
     if (!t->direct_va) {
-      e = cudaHostGetDevicePointer(&dp, const_cast<uint8_t*>(t->reg_base), 0);
-      if (e != cudaSuccess) return cuda_err(e, "cudaHostGetDevicePointer");
+      Pin pin;
+      pin.base = t->reg_base;
+      pin.len = t->reg_len;
+      if (pin_device_ptr(pin, t->host, &dev_base) != UT_OK) return UT_ECUDA;
     }
     unsigned long long* err = nullptr;
     e = cudaMalloc(&err, sizeof *err);
@@ -231,7 +319,7 @@ int dev_state(const ut_table* ct, DevState** out) {
     uint64_t keep = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     s->pool = pool;
-    s->dev_base = (uint64_t)dp + (uint64_t)(t->host - t->reg_base);
+    s->dev_base = dev_base;
     s->err = err;
     s->sms = sms > 0 ? sms : 148;
     s->init = true;
@@ -539,10 +627,6 @@ ut_table* ut_register(const void* host_ptr, uint64_t rows, uint64_t row_bytes) {
   cudaDeviceGetAttribute(&can_map, cudaDevAttrCanMapHostMemory, dev);
   if (!can_map) return set_err(UT_ENOTSUP, "device %d cannot map host memory", dev), nullptr;
 
-  const uint64_t pg = (uint64_t)sysconf(_SC_PAGESIZE);
-  const uint64_t lo = (uint64_t)host_ptr / pg * pg;
-  const uint64_t hi = ((uint64_t)host_ptr + bytes + pg - 1) / pg * pg;
-
   ut_table* t = new (std::nothrow) ut_table;
   if (!t) return set_err(UT_ENOMEM, "out of host memory"), nullptr;
   t->host = (const uint8_t*)host_ptr;
@@ -551,40 +635,17 @@ ut_table* ut_register(const void* host_ptr, uint64_t rows, uint64_t row_bytes) {
   t->bytes = bytes;
   t->device = dev;
 
-  // Already page-locked and mapped (cudaHostAlloc / a previous registration)? Adopt it.
-  cudaPointerAttributes attr{};
-  e = cudaPointerGetAttributes(&attr, host_ptr);
-  cudaPointerAttributes attr_end{};
-  cudaError_t e2 = cudaPointerGetAttributes(&attr_end, (const uint8_t*)host_ptr + bytes - 1);
-  if (e == cudaSuccess && e2 == cudaSuccess && attr.type == cudaMemoryTypeHost &&
-      attr_end.type == cudaMemoryTypeHost && attr.devicePointer != nullptr) {
-    t->reg_base = (const uint8_t*)host_ptr;
-    t->reg_len = bytes;
-    t->registered = 0;
-  } else {
-    cudaGetLastError();
-    int ro_ok = 0;
-    cudaDeviceGetAttribute(&ro_ok, cudaDevAttrHostRegisterReadOnlySupported, dev);
-    unsigned flags = cudaHostRegisterPortable | cudaHostRegisterMapped;
-    e = cudaErrorUnknown;
-    if (ro_ok) {
-      e = cudaHostRegister((void*)lo, hi - lo, flags | cudaHostRegisterReadOnly);
-      if (e == cudaSuccess) t->read_only = 1;
-      else cudaGetLastError();
-    }
-    if (e != cudaSuccess) e = cudaHostRegister((void*)lo, hi - lo, flags);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      delete t;
-      if (e == cudaErrorMemoryAllocation)
-        return set_err(UT_ENOMEM, "cudaHostRegister(%llu bytes): %s", (unsigned long long)(hi - lo),
-                       cudaGetErrorString(e)), nullptr;
-      return cuda_err(e, "cudaHostRegister"), nullptr;
-    }
-    t->reg_base = (const uint8_t*)lo;
-    t->reg_len = hi - lo;
-    t->registered = 1;
+  // Already page-locked and mapped (cudaHostAlloc / a previous registration)? Adopt it;
+  // otherwise pin the page-aligned range in place.
+  Pin pin;
+  if (pin_host(host_ptr, bytes, true, &pin) != UT_OK) {
+    delete t;
+    return nullptr;
   }
+  t->reg_base = pin.base;
+  t->reg_len = pin.len;
+  t->registered = pin.registered;
+  t->read_only = pin.read_only;
   const char* env = getenv("UT_PLAN");
   if (env && *env) {
     bool ok;

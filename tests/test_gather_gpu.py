@@ -44,7 +44,9 @@ def _gather_check(table, host_addr, rows, rb, idx, out_off=0, plan=None, stream=
 
 def test_paper_worked_example():
     g = json.load(open(os.path.join(GOLDEN, "paper_fig5_example.json")))
-    feat = np.array([[100 * i + j for j in range(11)] for i in range(5)], dtype=np.float32)
+    hb = workloads.HostBuffer(5 * 44)      # page-aligned: registration pins whole pages
+    feat = hb.array().view(np.float32).reshape(5, 11)
+    feat[:] = np.array([[100 * i + j for j in range(11)] for i in range(5)], dtype=np.float32)
     with ut.Table(feat) as t:
         assert (t.rows, t.row_bytes) == (5, 44)
         out = t[torch.tensor(g["idx"], device="cuda")]
@@ -145,9 +147,12 @@ def test_empty_single_last_duplicates_and_out_of_range():
         _gather_check(t, hb.addr, rows, rb, [-3])
         assert t.error_pos() == -1                    # cleared by the previous read
     hb.close()
-    with ut.Table(np.arange(8, dtype=np.uint8), 1, 8) as t:
+    hb = workloads.HostBuffer(8)
+    hb.array()[:] = np.arange(8, dtype=np.uint8)
+    with ut.Table(hb.array(), 1, 8) as t:
         out = t[torch.zeros(5, dtype=torch.int64, device="cuda")]
         assert (out.cpu().numpy() == np.arange(8)).all()
+    hb.close()
 
 
 @pytest.mark.parametrize("rb", [4, 400, 2408])
