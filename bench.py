@@ -357,7 +357,7 @@ def run_ut(args, spec, dist):
     stream = torch.cuda.current_stream()
     sampler = None
     if args.sample == "gpu":
-        sampler = GpuSampling(spec, rank, world, count, seed, ut, torch)
+        sampler = GpuSampling(spec, rank, world, count, seed, ut, torch, args.graph_indptr)
         lists = sampler.node_lists_for_accounting()
     idx_dev = [torch.from_numpy(l).to("cuda") for l in lists]
     max_n = max(l.size for l in lists)
@@ -403,7 +403,13 @@ def run_ut(args, spec, dist):
     dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for s in range(args.steps):
+    if sampler is not None and args.pipeline:
+        # sample minibatch k+1 (its own stream) while minibatch k is gathered: the whole loop is
+        # one timed region on the gather stream; every step writes > L2 (no flush, stated)
+        nbytes, ms = sampler.pipelined(args.warmup, args.steps, table, out)
+        e0 = e1 = None
+        evs = [ms]
+    for s in range(0 if (sampler is not None and args.pipeline) else args.steps):
         flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -422,7 +428,7 @@ def run_ut(args, spec, dist):
     clk = clocks.stop()
     st = table.stats(reset=True)
     table.set_plan("timing=off")
-    dev_ms = sum(a.elapsed_time(b) for a, b in evs)
+    dev_ms = evs[0] if (sampler is not None and args.pipeline) else sum(a.elapsed_time(b) for a, b in evs)
 
     value, max_dev_ms, max_wall, launches = box_throughput(dist, nbytes, dev_ms, wall,
                                                            st["kernel_launches"])
@@ -524,12 +530,14 @@ class GpuSampling:
     N and E (workloads.CSRGraph); each step's 'batch' roots are the rank's slice of a seeded
     permutation."""
 
-    def __init__(self, spec, rank, world, count, seed, ut, torch):
+    def __init__(self, spec, rank, world, count, seed, ut, torch, indptr="host"):
         assert spec["kind"] == "graphsage", "--sample gpu needs a graphsage-shaped config"
         self.torch, self.ut, self.spec = torch, ut, spec
         self.csr = workloads.CSRGraph(spec["rows"], spec["edges"], seed=seed, threads=0)
         self.graph = ut.Graph(self.csr.indptr_addr, self.csr.indices_addr, self.csr.n_nodes,
                               self.csr.n_edges, keep=self.csr)
+        self.graph.set_option(f"indptr={indptr}")
+        self.indptr = indptr
         perm = np.random.default_rng(seed + 99).permutation(spec["rows"])
         B = spec["batch"]
         self.roots = [perm[((b * world + rank) * B) % spec["rows"]:][:B].astype(np.int64)
@@ -565,6 +573,44 @@ class GpuSampling:
         self.rows += n
         return n
 
+    def pipelined(self, first, steps, table, out):
+        """Steps first..first+steps-1 with sampling of step k+1 overlapping the gather of step k
+        (two node buffers, two streams). Returns (useful bytes, elapsed ms on the gather side)."""
+        torch = self.torch
+        rb = self.spec["row_bytes"]
+        ss, sg = torch.cuda.Stream(), torch.cuda.Stream()
+        bufs = [self.nodes, torch.empty_like(self.nodes)]
+        sampled = [torch.cuda.Event(), torch.cuda.Event()]
+        gathered = [torch.cuda.Event(), torch.cuda.Event()]
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        nb = len(self.roots_dev)
+        with torch.cuda.stream(ss):
+            nodes = [self.graph.sample(self.roots_dev[first % nb], self.fanouts,
+                                       self.seed + first % nb, out=bufs[0], stream=ss), None]
+            sampled[0].record(ss)
+        total = 0
+        start.record(sg)
+        for k in range(steps):
+            cur, nxt = k % 2, (k + 1) % 2
+            sg.wait_event(sampled[cur])
+            n = nodes[cur].numel()
+            with torch.cuda.stream(sg):
+                table.gather(nodes[cur], out=out[: n * rb], stream=sg)
+            gathered[cur].record(sg)
+            total += n * rb
+            if k + 1 < steps:
+                b = (first + k + 1) % nb
+                ss.wait_event(gathered[nxt])
+                with torch.cuda.stream(ss):
+                    nodes[nxt] = self.graph.sample(self.roots_dev[b], self.fanouts, self.seed + b,
+                                                   out=bufs[nxt], stream=ss)
+                    sampled[nxt].record(ss)
+        end.record(sg)
+        torch.cuda.synchronize()
+        self.rows += total // rb
+        return total, start.elapsed_time(end)
+
     def check(self, table_addr, table, out) -> bool:
         import oracle
         r = self.roots[0]
@@ -582,7 +628,7 @@ class GpuSampling:
         import time as _t
         import oracle
         self.torch.cuda.synchronize()
-        ms = [a.elapsed_time(b) for a, b in self.mid[-steps:]]
+        ms = [a.elapsed_time(b) for a, b in self.mid[-steps:]] or [float("nan")]
         t0 = _t.perf_counter()
         for b in range(3):
             oracle.sample(self.csr.indptr_addr, self.csr.indices_addr, self.csr.n_nodes,
@@ -590,7 +636,9 @@ class GpuSampling:
         cpu_ms = (_t.perf_counter() - t0) / 3 * 1e3
         return {"where": "gpu (ut_sample over the host-resident CSR), inside every timed step",
                 "graph": f"explicit Chung-Lu CSR, N={self.csr.n_nodes}, E={self.csr.n_edges}",
+                "indptr": self.indptr, "pipelined": bool(self.rows and not self.mid[steps:]),
                 "gpu_sample_ms_per_step": round(float(np.mean(ms)), 3),
+                "gpu_sample_ms_measured_on": "non-overlapped steps (warm-up when --pipeline)",
                 "oracle_cpu_sample_ms_per_minibatch": round(cpu_ms, 2), "oracle_cores": 1}
 
 
@@ -641,6 +689,10 @@ def main(argv=None):
     ap.add_argument("--sample", default="cpu", choices=["cpu", "gpu"],
                     help="cpu: index lists sampled before timing (default, the paper's split); "
                          "gpu: ut_sample inside every timed step (SURVEY NEXT-2)")
+    ap.add_argument("--graph-indptr", default="host", choices=["host", "hbm"],
+                    help="with --sample gpu: CSR indptr read over the link or copied to HBM")
+    ap.add_argument("--pipeline", action="store_true",
+                    help="with --sample gpu: sample minibatch k+1 while gathering minibatch k")
     ap.add_argument("--allreduce-smoke", action="store_true",
                     help="N > 1: one untimed NCCL all-reduce of a 4-MB fp32 buffer after timing")
     args = ap.parse_args(argv)
