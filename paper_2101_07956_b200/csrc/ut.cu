@@ -328,14 +328,11 @@ int dev_state(const ut_table* ct, DevState** out) {
   return UT_OK;
 }
 
-// Resident gather blocks per SM (256 threads each). Two (16 warps) already saturate the link
-// for every row width measured (products 45.3 vs 45.2 GB/s at full occupancy, 256-B rows 49.7
-// vs 48.3), and leave most of each SM to concurrent kernels — the sampler of the next minibatch,
-// or the training step that consumes the rows. UT_BLOCKS_PER_SM overrides (0 = occupancy max).
+// Resident gather blocks per SM (256 threads each), env override UT_BLOCKS_PER_SM (0 = max).
 int blocks_per_sm_cap() {
   static const int cap = [] {
     const char* e = getenv("UT_BLOCKS_PER_SM");
-    return (e && *e) ? atoi(e) : 2;
+    return (e && *e) ? atoi(e) : -1;
   }();
   return cap;
 }
@@ -346,13 +343,14 @@ int grid_for(K kernel, int sms, uint64_t work_warps, int cap_blocks = 0) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
   if (per_sm <= 0) per_sm = 1;
   if (blocks_per_sm_cap() > 0) per_sm = std::min(per_sm, blocks_per_sm_cap());
+  else if (blocks_per_sm_cap() < 0 && cap_blocks < 0) per_sm = std::min(per_sm, -cap_blocks);
   uint64_t full = (uint64_t)sms * per_sm;
   static const int max_blocks = [] {
     const char* e = getenv("UT_MAX_BLOCKS");        // A/B knob: cap the gather grid
     return (e && *e) ? atoi(e) : 0;
   }();
   if (max_blocks > 0) full = std::min<uint64_t>(full, (uint64_t)max_blocks);
-  if (cap_blocks > 0) full = std::min<uint64_t>(full, (uint64_t)cap_blocks);
+  if (cap_blocks > 0) full = std::min<uint64_t>(full, (uint64_t)cap_blocks);   // < 0: per SM
   uint64_t need = (work_warps + 7) / 8;
   return (int)std::max<uint64_t>(1, std::min(full, need));
 }
@@ -403,15 +401,19 @@ cudaError_t launch_single_u(const Plan& p, int sms, cudaStream_t st, const ut::G
 
 template <int G, bool PERM>
 cudaError_t launch_single(const Plan& p, int sms, cudaStream_t st, const ut::GatherArgs& a,
-                          const Shape& sh) {
+                          const Shape& sh, int cap) {
   if (PERM && sh.sparse) return launch_single_u<G, 1, PERM>(p, sms, st, a, sh.cap_blocks);
-  return launch_single_u<G, kU, PERM>(p, sms, st, a, 0);
+  return launch_single_u<G, kU, PERM>(p, sms, st, a, cap);
 }
 
+// Dense shape: rows > 128 B are link-bound with 2 resident blocks (16 warps) per SM (products
+// 45.3 vs 45.2 GB/s at full occupancy, 256-B rows 49.7 vs 48.3) — the rest of each SM stays
+// free for concurrent kernels (the next minibatch's sampler, the training step). Rows <= 128 B
+// are request-rate-bound and keep every resident block (128-B rows 29.8 vs 27.7 GB/s).
 template <bool PERM>
 cudaError_t launch_plan(const Plan& p, int sms, cudaStream_t st, const ut::GatherArgs& a,
                         const Shape& sh) {
-  const int cap = sh.sparse ? sh.cap_blocks : 0;
+  const int cap = sh.sparse ? sh.cap_blocks : (a.rb > 128 ? -2 : 0);
   switch (p.kind) {
     case P_NARROW: {
       const uint64_t warps = (a.n + 32 * kUn - 1) / (32 * kUn);
@@ -425,12 +427,12 @@ cudaError_t launch_plan(const Plan& p, int sms, cudaStream_t st, const ut::Gathe
     case P_VEC16:
     case P_REALIGN:
       switch (p.g) {
-        case 1: return launch_single<1, PERM>(p, sms, st, a, sh);
-        case 2: return launch_single<2, PERM>(p, sms, st, a, sh);
-        case 4: return launch_single<4, PERM>(p, sms, st, a, sh);
-        case 8: return launch_single<8, PERM>(p, sms, st, a, sh);
-        case 16: return launch_single<16, PERM>(p, sms, st, a, sh);
-        default: return launch_single<32, PERM>(p, sms, st, a, sh);
+        case 1: return launch_single<1, PERM>(p, sms, st, a, sh, cap);
+        case 2: return launch_single<2, PERM>(p, sms, st, a, sh, cap);
+        case 4: return launch_single<4, PERM>(p, sms, st, a, sh, cap);
+        case 8: return launch_single<8, PERM>(p, sms, st, a, sh, cap);
+        case 16: return launch_single<16, PERM>(p, sms, st, a, sh, cap);
+        default: return launch_single<32, PERM>(p, sms, st, a, sh, cap);
       }
     case P_VEC16X: {
       auto k = ut::k_multi<kUx, true, false, PERM>;
