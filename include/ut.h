@@ -191,6 +191,19 @@ UT_API const char* ut_plan_probe(uint64_t base, uint64_t rows, uint64_t row_byte
  */
 UT_API int ut_set_plan(ut_table* t, const char* name);
 
+/*
+ * ut_mem_advise — the paper's `unified_tensor.memAdvise(advise, adviseDevice)` (Table 2,
+ * PAPER.md:413-416, 440-450): apply cudaMemAdvise to the table's storage and return the CUDA
+ * error code as an int (0 = cudaSuccess) — "Invoke cudaMemAdvise and returns error code".
+ *   advice  0 SetPreferredLocation, 1 UnsetPreferredLocation, 2 SetAccessedBy,
+ *           3 UnsetAccessedBy, 4 SetReadMostly, 5 UnsetReadMostly.
+ *   device  -1 = the CPU (host), >= 0 = that GPU.
+ * Meaningful for managed tables (ut_create UT_ALLOC_MANAGED); pinned memory returns the runtime's
+ * error code (cudaErrorInvalidValue) unchanged. Returns UT_EINVAL (negative) for a NULL table or
+ * an unknown advice.
+ */
+UT_API int ut_mem_advise(const ut_table* t, int advice, int device);
+
 /* ---- GPU-side neighbour sampling over a host-resident CSR graph -------------
  * The step before the gather that the paper leaves on the CPU. The CSR stays in
  * host memory (pinned in place like a feature table) and GPU threads read it over the link. */

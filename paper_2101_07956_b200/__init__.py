@@ -29,7 +29,7 @@ UT_OK, UT_EINVAL, UT_ENOMEM, UT_ECUDA, UT_ERANGE, UT_ENOTSUP = 0, -1, -2, -3, -4
 ABI = ("ut_register", "ut_gather", "ut_gather_host", "ut_release", "ut_error_pos",
        "ut_last_error", "ut_plan_name", "ut_plan_probe", "ut_set_plan", "ut_table_get_info",
        "ut_get_stats", "ut_create", "ut_graph_register", "ut_graph_set_option", "ut_sample",
-       "ut_graph_release")
+       "ut_graph_release", "ut_mem_advise")
 
 UT_ALLOC = {"pinned": 0, "managed": 1, "vmm": 2}
 
@@ -87,6 +87,8 @@ def _load():
     L.ut_sample.restype = ctypes.c_int
     L.ut_sample.argtypes = [vp, vp, u64, vp, ctypes.c_int, u64, vp, u64,
                             ctypes.POINTER(ctypes.c_uint64), vp]
+    L.ut_mem_advise.restype = ctypes.c_int
+    L.ut_mem_advise.argtypes = [vp, ctypes.c_int, ctypes.c_int]
     L.ut_graph_release.restype = ctypes.c_int
     L.ut_graph_release.argtypes = [vp]
     L.ut_get_stats.restype = ctypes.c_int
@@ -196,6 +198,14 @@ def ut_sample(g: int, seeds_dev: int, n_seeds: int, fanouts, seed: int, nodes_de
         code, msg = last_error()
         raise UTError(rc, msg)
     return int(n.value)
+
+
+def ut_mem_advise(t: int, advice: int, device: int) -> int:
+    """cudaMemAdvise on the table's storage; returns the CUDA error code (0 = success)."""
+    rc = _lib.ut_mem_advise(t, advice, device)
+    if rc < 0:
+        _check(rc)
+    return rc
 
 
 def ut_graph_release(g: int) -> None:

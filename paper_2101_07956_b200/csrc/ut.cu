@@ -1102,6 +1102,26 @@ int ut_get_stats(const ut_table* t, ut_stats* st, int reset) {
   return UT_OK;
 }
 
+int ut_mem_advise(const ut_table* t, int advice, int device) {
+  if (!t) return set_err(UT_EINVAL, "table is NULL");
+  static const cudaMemoryAdvise kinds[] = {
+      cudaMemAdviseSetPreferredLocation, cudaMemAdviseUnsetPreferredLocation,
+      cudaMemAdviseSetAccessedBy,        cudaMemAdviseUnsetAccessedBy,
+      cudaMemAdviseSetReadMostly,        cudaMemAdviseUnsetReadMostly};
+  if (advice < 0 || advice > 5) return set_err(UT_EINVAL, "unknown advice %d", advice);
+  cudaMemLocation loc{};
+  if (device < 0) {
+    loc.type = cudaMemLocationTypeHost;
+    loc.id = 0;
+  } else {
+    loc.type = cudaMemLocationTypeDevice;
+    loc.id = device;
+  }
+  cudaError_t e = cudaMemAdvise(t->host, t->bytes, kinds[advice], loc);
+  cudaGetLastError();
+  return (int)e;
+}
+
 int ut_table_get_info(const ut_table* t, ut_table_info* info) {
   if (!t || !info) return set_err(UT_EINVAL, "NULL argument");
   info->rows = t->rows;
