@@ -236,7 +236,7 @@ PlanKind parse_plan(const char* s, bool* ok) {
 }
 
 struct DevState {
-  bool init = false;
+  std::atomic<bool> init{false};       // published after the fields below are set
   uint64_t dev_base = 0;               // device address of the table on this device
   unsigned long long* err = nullptr;   // first out-of-range position, ~0 = none
   int sms = 0;
@@ -289,7 +289,7 @@ int dev_state(const ut_table* ct, DevState** out) {
   if (e != cudaSuccess) return cuda_err(e, "cudaGetDevice");
   if (dev < 0 || dev >= kMaxDev) return set_err(UT_ENOTSUP, "device %d beyond %d", dev, kMaxDev);
   DevState* s = &t->dev[dev];
-  if (s->init) {
+  if (s->init.load(std::memory_order_acquire)) {
     *out = s;
     return UT_OK;
   }
@@ -322,7 +322,7 @@ int dev_state(const ut_table* ct, DevState** out) {
     s->dev_base = dev_base;
     s->err = err;
     s->sms = sms > 0 ? sms : 148;
-    s->init = true;
+    s->init.store(true, std::memory_order_release);
   }
   *out = s;
   return UT_OK;

@@ -1,0 +1,50 @@
+"""Tiny cases for compute-sanitizer (memcheck / racecheck / synccheck): every kernel family,
+the reorder stage, the TMA bulk plan, the paper's kernels, host end-to-end and GPU sampling."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import oracle
+import paper_2101_07956_b200 as ut
+import workloads
+
+bad = 0
+for rb, off in [(4, 0), (8, 8), (68, 3), (400, 0), (400, 4), (2052, 1), (4096, 0), (13, 5)]:
+    rows = 3000
+    hb = workloads.HostBuffer(rows * rb, kind="guarded")
+    workloads.fill_table(hb.addr, rows, rb, rb)
+    idx = workloads.uniform_idx(700, rows, rb)
+    idx[:2] = [0, rows - 1]
+    want, _ = oracle.gather(hb.addr, rows, rb, idx)
+    with ut.Table(hb.addr, rows, rb) as t:
+        for plan in ["auto", "realign", "realignx", "vec16", "vec16x", "narrow", "bulk",
+                     "paper_naive", "paper_shift"]:
+            try:
+                t.set_plan(plan)
+            except ut.UTError:
+                continue
+            for reorder in ["reorder=off", "reorder=on"]:
+                t.set_plan(reorder)
+                buf = torch.zeros(700 * rb + 16, dtype=torch.uint8, device="cuda")
+                t.gather(torch.from_numpy(idx).cuda(), out=buf[off: off + 700 * rb])
+                got = buf[off: off + 700 * rb].cpu().numpy()
+                if got.tobytes() != want.tobytes():
+                    bad += 1
+                    print("MISMATCH", rb, plan, reorder)
+        t.set_plan("auto")
+        t.set_plan("reorder=auto")
+        o = t.gather_host(torch.from_numpy(idx).pin_memory())
+        bad += o.numpy().tobytes() != want.tobytes()
+    hb.close()
+
+g = workloads.CSRGraph(20000, 300000, seed=4)
+with ut.Graph(g.indptr_addr, g.indices_addr, g.n_nodes, g.n_edges, keep=g) as gr:
+    seeds = np.arange(0, 20000, 97, dtype=np.int64)
+    got = gr.sample(torch.from_numpy(seeds).cuda(), [5, 3], 11).cpu().numpy()
+    want = oracle.sample(g.indptr_addr, g.indices_addr, g.n_nodes, seeds, [5, 3], 11)
+    bad += not np.array_equal(got, want)
+torch.cuda.synchronize()
+print("SANITIZE-CASES-DONE bad=%d" % bad)
