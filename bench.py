@@ -357,7 +357,8 @@ def run_ut(args, spec, dist):
     stream = torch.cuda.current_stream()
     sampler = None
     if args.sample == "gpu":
-        sampler = GpuSampling(spec, rank, world, count, seed, ut, torch, args.graph_indptr)
+        sampler = GpuSampling(spec, rank, world, count, seed, ut, torch, args.graph_indptr,
+                              "graph" if args.graph else "async" if args.async_sample else "sync")
         lists = sampler.node_lists_for_accounting()
     idx_dev = [torch.from_numpy(l).to("cuda") for l in lists]
     max_n = max(l.size for l in lists)
@@ -395,9 +396,13 @@ def run_ut(args, spec, dist):
         l = idx_dev[s % count]
         table.gather(l, out=out[: l.numel() * rb])
     torch.cuda.synchronize()
+    if sampler is not None and sampler.mode != "sync":
+        sampler.device_rows()          # drop the warm-up counts
 
     table.set_plan("timing=on")
     table.stats(reset=True)
+    if sampler is not None:
+        sampler.mark()
     evs = []
     nbytes = 0
     dist.barrier()
@@ -423,6 +428,8 @@ def run_ut(args, spec, dist):
         e1.record(stream)
         evs.append((e0, e1))
     torch.cuda.synchronize()
+    if sampler is not None and sampler.mode != "sync":
+        nbytes += sampler.device_rows() * rb
     dist.barrier()
     wall = time.perf_counter() - t0
     clk = clocks.stop()
@@ -430,12 +437,15 @@ def run_ut(args, spec, dist):
     table.set_plan("timing=off")
     dev_ms = evs[0] if (sampler is not None and args.pipeline) else sum(a.elapsed_time(b) for a, b in evs)
 
+    own_launches = st["kernel_launches"]
+    if sampler is not None:
+        own_launches += sampler.timed_launches(args.steps)
     value, max_dev_ms, max_wall, launches = box_throughput(dist, nbytes, dev_ms, wall,
-                                                           st["kernel_launches"])
+                                                           own_launches)
     per_gpu = nbytes / (dev_ms / 1e3) / 1e9
     kern_ms = st["gather_kernel_ms"] / max(1, st["timed_launches"])
     kern_bytes = nbytes / max(1, st["timed_launches"])
-    achieved = kern_bytes / (kern_ms / 1e3) / 1e9 if kern_ms > 0 else 0.0
+    achieved = kern_bytes / (kern_ms / 1e3) / 1e9 if kern_ms > 0 else None   # None: graph replay
 
     # end to end: host idx in (pinned), host rows out (pinned), through ut_gather_host
     e2e = None
@@ -502,9 +512,11 @@ def run_ut(args, spec, dist):
             "box_roofline_gbs": round(min(link_sum, dram), 3) if dram else round(link_sum, 3),
             "frac_of_link": round(per_gpu / link, 4),
             "plan": table.plan, "table_memory": args.alloc,
-            "roofline": {"bound": "pcie_h2d", "achieved": round(achieved, 3),
+            "roofline": {"bound": "pcie_h2d",
+                         "achieved": round(achieved, 3) if achieved is not None else None,
                          "peak": round(link, 3), "unit": "GB/s",
-                         "frac": round(achieved / link, 4), "traffic": None,
+                         "frac": round(achieved / link, 4) if achieved is not None else None,
+                         "traffic": None,
                          "kernel": f"gather {table.plan} (device time of the gather kernel alone, CUDA events on its stream)",
                          "peak_source": "pinned cudaMemcpy H2D measured in this run (best of 10 x 1 GiB)"},
             "cpu_baseline": cpu_base, "py_baseline": py_base, "e2e": e2e,
@@ -530,7 +542,7 @@ class GpuSampling:
     N and E (workloads.CSRGraph); each step's 'batch' roots are the rank's slice of a seeded
     permutation."""
 
-    def __init__(self, spec, rank, world, count, seed, ut, torch, indptr="host"):
+    def __init__(self, spec, rank, world, count, seed, ut, torch, indptr="host", mode="sync"):
         assert spec["kind"] == "graphsage", "--sample gpu needs a graphsage-shaped config"
         self.torch, self.ut, self.spec = torch, ut, spec
         self.csr = workloads.CSRGraph(spec["rows"], spec["edges"], seed=seed, threads=0)
@@ -550,6 +562,14 @@ class GpuSampling:
             cap += cap * f
         self.nodes = torch.empty(min(cap, spec["rows"]), dtype=torch.int64, device="cuda")
         self.ms_sample, self.rows, self.mid = 0.0, 0, []
+        self.mode = mode
+        self.seeds_buf = torch.empty(B, dtype=torch.int64, device="cuda")
+        self.n_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.counts = torch.zeros(4096, dtype=torch.int64, device="cuda")
+        self.k = 0
+        self.cuda_graph = None
+        self.graph_kernels = 0
+        self._l_mark = 0
 
     def node_lists_for_accounting(self):
         """The minibatches' node lists, computed on the GPU once (for the traffic model and the
@@ -560,17 +580,63 @@ class GpuSampling:
         return out
 
     def step(self, s, table, out):
+        """One minibatch: sample on the GPU, then gather its rows. Synchronous API (one host
+        sync per minibatch to learn the count) unless --async-sample: then ut_sample_async +
+        ut_gather_dn keep the count on the device (no host sync), optionally replayed from a
+        CUDA graph captured once (--graph). Returns rows gathered (host-known modes) or 0."""
         torch = self.torch
         b = s % len(self.roots_dev)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        nodes = self.graph.sample(self.roots_dev[b], self.fanouts, self.seed + b, out=self.nodes)
-        e1.record()
-        self.mid.append((e0, e1))
-        n = nodes.numel()
-        table.gather(nodes, out=out[: n * self.spec["row_bytes"]])
-        self.rows += n
+        if self.mode == "sync":
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            nodes = self.graph.sample(self.roots_dev[b], self.fanouts, self.seed + b, out=self.nodes)
+            e1.record()
+            self.mid.append((e0, e1))
+            n = nodes.numel()
+            table.gather(nodes, out=out[: n * self.spec["row_bytes"]])
+            self.rows += n
+            return n
+        self.seeds_buf.copy_(self.roots_dev[b])
+        if self.mode == "graph":
+            if self.cuda_graph is None:
+                self._capture(table, out)
+            self.cuda_graph.replay()
+        else:
+            self.graph.sample_async(self.seeds_buf, self.fanouts, self.seed, self.nodes, self.n_dev)
+            table.gather_dn(self.nodes, self.n_dev, out)
+        self.counts[self.k % self.counts.numel()].copy_(self.n_dev[0])
+        self.k += 1
+        return 0
+
+    def _capture(self, table, out):
+        torch = self.torch
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        self.cuda_graph = torch.cuda.CUDAGraph()
+        l0 = self.graph.launches() + table.stats()["kernel_launches"]
+        with torch.cuda.graph(self.cuda_graph, stream=st):
+            self.graph.sample_async(self.seeds_buf, self.fanouts, self.seed, self.nodes, self.n_dev,
+                                    stream=st)
+            table.gather_dn(self.nodes, self.n_dev, out, stream=st)
+        torch.cuda.current_stream().wait_stream(st)
+        self.graph_kernels = self.graph.launches() + table.stats()["kernel_launches"] - l0
+
+    def timed_launches(self, steps) -> int:
+        """Sampler kernels in the timed region (graph replays: the captured count x steps)."""
+        if self.mode == "graph":
+            return self.graph_kernels * steps
+        n = self.graph.launches() - self._l_mark
+        return n
+
+    def mark(self):
+        self._l_mark = self.graph.launches()
+
+    def device_rows(self) -> int:
+        """Rows gathered by the device-counted steps since the last call."""
+        k = min(self.k, self.counts.numel())
+        n = int(self.counts[:k].sum().item())
+        self.k = 0
         return n
 
     def pipelined(self, first, steps, table, out):
@@ -628,7 +694,17 @@ class GpuSampling:
         import time as _t
         import oracle
         self.torch.cuda.synchronize()
-        ms = [a.elapsed_time(b) for a, b in self.mid[-steps:]] or [float("nan")]
+        ms = [a.elapsed_time(b) for a, b in self.mid[-steps:]]
+        if not ms:      # device-counted modes: time the sampler alone on a few minibatches
+            for b in range(min(5, len(self.roots_dev))):
+                self.seeds_buf.copy_(self.roots_dev[b])
+                e0 = self.torch.cuda.Event(enable_timing=True)
+                e1 = self.torch.cuda.Event(enable_timing=True)
+                e0.record()
+                self.graph.sample_async(self.seeds_buf, self.fanouts, self.seed, self.nodes, self.n_dev)
+                e1.record()
+                self.torch.cuda.synchronize()
+                ms.append(e0.elapsed_time(e1))
         t0 = _t.perf_counter()
         for b in range(3):
             oracle.sample(self.csr.indptr_addr, self.csr.indices_addr, self.csr.n_nodes,
@@ -636,9 +712,9 @@ class GpuSampling:
         cpu_ms = (_t.perf_counter() - t0) / 3 * 1e3
         return {"where": "gpu (ut_sample over the host-resident CSR), inside every timed step",
                 "graph": f"explicit Chung-Lu CSR, N={self.csr.n_nodes}, E={self.csr.n_edges}",
-                "indptr": self.indptr, "pipelined": bool(self.rows and not self.mid[steps:]),
+                "indptr": self.indptr, "mode": self.mode,
                 "gpu_sample_ms_per_step": round(float(np.mean(ms)), 3),
-                "gpu_sample_ms_measured_on": "non-overlapped steps (warm-up when --pipeline)",
+                "gpu_sample_ms_measured_on": "timed steps (sync mode) or 5 standalone async samples",
                 "oracle_cpu_sample_ms_per_minibatch": round(cpu_ms, 2), "oracle_cores": 1}
 
 
@@ -691,6 +767,10 @@ def main(argv=None):
                          "gpu: ut_sample inside every timed step (SURVEY NEXT-2)")
     ap.add_argument("--graph-indptr", default="host", choices=["host", "hbm"],
                     help="with --sample gpu: CSR indptr read over the link or copied to HBM")
+    ap.add_argument("--async-sample", action="store_true",
+                    help="with --sample gpu: ut_sample_async + ut_gather_dn (no host sync)")
+    ap.add_argument("--graph", action="store_true",
+                    help="with --sample gpu: capture sample + gather once in a CUDA graph, replay")
     ap.add_argument("--pipeline", action="store_true",
                     help="with --sample gpu: sample minibatch k+1 while gathering minibatch k")
     ap.add_argument("--allreduce-smoke", action="store_true",

@@ -126,6 +126,15 @@ UT_API int ut_gather(const ut_table* t, const int64_t* idx_dev, uint64_t n, void
               ut_stream_t stream);
 
 /*
+ * ut_gather_dn — ut_gather whose row count lives in device memory: gathers
+ * min(*n_dev, max_n) rows, read by the kernels themselves, so a device-side producer of the index
+ * list (ut_sample_async) and this gather need no host synchronisation between them and can be
+ * captured in one CUDA graph. Launch sizes follow max_n (< 2^31). Errors as ut_gather.
+ */
+UT_API int ut_gather_dn(const ut_table* t, const int64_t* idx_dev, const uint64_t* n_dev,
+                        uint64_t max_n, void* out_dev, ut_stream_t stream);
+
+/*
  * ut_gather_host — the same gather from and to HOST buffers (the end-to-end form).
  *   idx_host  n int64 row ids in host memory (page-locked for full speed; caller-owned).
  *   out_host  >= n*rb bytes of host memory (caller-owned).
@@ -235,12 +244,35 @@ UT_API int ut_graph_set_option(ut_graph* g, const char* option);
  *   nodes_dev  device int64[cap]: receives the final frontier (the minibatch's node list, seeds
  *              first) — the index list a following ut_gather reads.
  *   *n_out     node count (set even when cap is too small, then UT_EINVAL is returned).
- * Synchronises `stream` twice per hop to read sizes; the nodes are written stream-ordered.
- * Returns UT_OK, UT_EINVAL, UT_ERANGE (a seed outside [0, n_nodes)), UT_ENOMEM or UT_ECUDA.
+ * Synchronises `stream` once, at the end, to return the count (the sampler itself keeps every
+ * size in device memory). Returns UT_OK, UT_EINVAL, UT_ERANGE (a seed outside [0, n_nodes); such
+ * seeds are dropped), UT_ENOMEM or UT_ECUDA.
  */
 UT_API int ut_sample(ut_graph* g, const int64_t* seeds_dev, uint64_t n_seeds, const int32_t* fanouts,
                      int n_hops, uint64_t seed, int64_t* nodes_dev, uint64_t cap, uint64_t* n_out,
                      ut_stream_t stream);
+
+/*
+ * ut_sample_capacity — the worst-case node count of a call: min(n_nodes, n_seeds * prod(1 + f_h)).
+ * ut_sample_async needs nodes_dev to hold this many entries.
+ */
+UT_API uint64_t ut_sample_capacity(uint64_t n_seeds, const int32_t* fanouts, int n_hops,
+                                   uint64_t n_nodes);
+
+/*
+ * ut_sample_async — ut_sample with no host synchronisation: every launch is sized by the
+ * worst case and reads the live sizes from device memory; the node count is written to the
+ * device word *n_out_dev. cap must be >= ut_sample_capacity(...). Seeds outside [0, n_nodes) are
+ * dropped silently. With ut_gather_dn(t, nodes_dev, n_out_dev, cap, ...) on the same stream, a
+ * whole minibatch (sample + gather) is host-sync-free and can be captured in a CUDA graph;
+ * replays re-read the seeds buffer. Returns UT_OK, UT_EINVAL, UT_ENOMEM or UT_ECUDA.
+ */
+UT_API int ut_sample_async(ut_graph* g, const int64_t* seeds_dev, uint64_t n_seeds,
+                           const int32_t* fanouts, int n_hops, uint64_t seed, int64_t* nodes_dev,
+                           uint64_t cap, uint64_t* n_out_dev, ut_stream_t stream);
+
+/* Kernels enqueued by ut_sample / ut_sample_async on this graph so far (for launch counts). */
+UT_API uint64_t ut_graph_launches(const ut_graph* g);
 
 /* Free the sampler state and unpin the CSR arrays (if ut_graph_register pinned them). */
 UT_API int ut_graph_release(ut_graph* g);

@@ -29,7 +29,8 @@ UT_OK, UT_EINVAL, UT_ENOMEM, UT_ECUDA, UT_ERANGE, UT_ENOTSUP = 0, -1, -2, -3, -4
 ABI = ("ut_register", "ut_gather", "ut_gather_host", "ut_release", "ut_error_pos",
        "ut_last_error", "ut_plan_name", "ut_plan_probe", "ut_set_plan", "ut_table_get_info",
        "ut_get_stats", "ut_create", "ut_graph_register", "ut_graph_set_option", "ut_sample",
-       "ut_graph_release", "ut_mem_advise")
+       "ut_graph_release", "ut_mem_advise", "ut_gather_dn", "ut_sample_async",
+       "ut_sample_capacity", "ut_graph_launches")
 
 UT_ALLOC = {"pinned": 0, "managed": 1, "vmm": 2}
 
@@ -87,6 +88,14 @@ def _load():
     L.ut_sample.restype = ctypes.c_int
     L.ut_sample.argtypes = [vp, vp, u64, vp, ctypes.c_int, u64, vp, u64,
                             ctypes.POINTER(ctypes.c_uint64), vp]
+    L.ut_gather_dn.restype = ctypes.c_int
+    L.ut_gather_dn.argtypes = [vp, vp, vp, u64, vp, vp]
+    L.ut_sample_async.restype = ctypes.c_int
+    L.ut_sample_async.argtypes = [vp, vp, u64, vp, ctypes.c_int, u64, vp, u64, vp, vp]
+    L.ut_sample_capacity.restype = ctypes.c_uint64
+    L.ut_sample_capacity.argtypes = [u64, vp, ctypes.c_int, u64]
+    L.ut_graph_launches.restype = ctypes.c_uint64
+    L.ut_graph_launches.argtypes = [vp]
     L.ut_mem_advise.restype = ctypes.c_int
     L.ut_mem_advise.argtypes = [vp, ctypes.c_int, ctypes.c_int]
     L.ut_graph_release.restype = ctypes.c_int
@@ -208,6 +217,22 @@ def ut_mem_advise(t: int, advice: int, device: int) -> int:
     return rc
 
 
+def ut_gather_dn(t: int, idx_dev: int, n_dev: int, max_n: int, out_dev: int, stream: int = 0) -> None:
+    _check(_lib.ut_gather_dn(t, idx_dev, n_dev, max_n, out_dev, stream))
+
+
+def ut_sample_capacity(n_seeds: int, fanouts, n_nodes: int) -> int:
+    fan = (ctypes.c_int32 * max(1, len(fanouts)))(*fanouts)
+    return int(_lib.ut_sample_capacity(n_seeds, fan, len(fanouts), n_nodes))
+
+
+def ut_sample_async(g: int, seeds_dev: int, n_seeds: int, fanouts, seed: int, nodes_dev: int,
+                    cap: int, n_out_dev: int, stream: int = 0) -> None:
+    fan = (ctypes.c_int32 * max(1, len(fanouts)))(*fanouts)
+    _check(_lib.ut_sample_async(g, seeds_dev, n_seeds, fan, len(fanouts),
+                                seed & 0xFFFFFFFFFFFFFFFF, nodes_dev, cap, n_out_dev, stream))
+
+
 def ut_graph_release(g: int) -> None:
     _check(_lib.ut_graph_release(g))
 
@@ -297,6 +322,12 @@ class Table:
 
     __getitem__ = gather
 
+    def gather_dn(self, idx, n_dev, out, stream=None):
+        """Gather min(n_dev[0], idx.numel()) rows; the count is read on the device."""
+        ut_gather_dn(self.handle, idx.data_ptr(), n_dev.data_ptr(), idx.numel(), out.data_ptr(),
+                     _stream_handle(stream))
+        return out
+
     def gather_host(self, idx_host, out_host=None, stream=None):
         """End-to-end form: host int64 idx in, host rows out (uint8 [n, row_bytes])."""
         import torch
@@ -356,6 +387,18 @@ class Graph:
         n = ut_sample(self.handle, seeds.data_ptr(), seeds.numel(), list(fanouts), seed,
                       out.data_ptr(), out.numel(), _stream_handle(stream))
         return out[:n]
+
+    def launches(self) -> int:
+        return int(_lib.ut_graph_launches(self.handle))
+
+    def capacity(self, n_seeds: int, fanouts) -> int:
+        return ut_sample_capacity(n_seeds, list(fanouts), self.n_nodes)
+
+    def sample_async(self, seeds, fanouts, seed: int, nodes, n_dev, stream=None) -> None:
+        """Enqueue a sample into `nodes` (CUDA int64, >= capacity) and its count into `n_dev`
+        (CUDA int64 [1]) with no host synchronisation (graph-capturable)."""
+        ut_sample_async(self.handle, seeds.data_ptr(), seeds.numel(), list(fanouts), seed,
+                        nodes.data_ptr(), nodes.numel(), n_dev.data_ptr(), _stream_handle(stream))
 
     def close(self) -> None:
         if getattr(self, "handle", None):

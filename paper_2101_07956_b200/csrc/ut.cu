@@ -500,12 +500,12 @@ int bucket_shift(uint64_t table_bytes, uint64_t rb) {
 }
 
 int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n, void* out_dev,
-              cudaStream_t st, bool host_out = false) {
+              cudaStream_t st, bool host_out = false, const uint64_t* n_dev = nullptr) {
   Plan p;
   if (!choose_plan((uint64_t)t->host, t->rows, t->rb, (uint64_t)out_dev, t->forced, &p) &&
       !choose_plan((uint64_t)t->host, t->rows, t->rb, (uint64_t)out_dev, P_AUTO, &p))
     return set_err(UT_EINVAL, "no admissible plan");
-  ut::GatherArgs a{s->dev_base, t->rows, t->rb, idx_dev, n, (uint64_t)out_dev, s->err, nullptr};
+  ut::GatherArgs a{s->dev_base, t->rows, t->rb, idx_dev, n, (uint64_t)out_dev, s->err, nullptr, n_dev};
   cudaError_t e;
   s->rows += n;
   s->bytes += n * t->rb;
@@ -848,6 +848,19 @@ int ut_gather(const ut_table* t, const int64_t* idx_dev, uint64_t n, void* out_d
   int rc = dev_state(t, &s);
   if (rc != UT_OK) return rc;
   return gather_on(t, s, idx_dev, n, out_dev, (cudaStream_t)stream);
+}
+
+int ut_gather_dn(const ut_table* t, const int64_t* idx_dev, const uint64_t* n_dev, uint64_t max_n,
+                 void* out_dev, ut_stream_t stream) {
+  if (!t || !n_dev) return set_err(UT_EINVAL, "table or n_dev is NULL");
+  if (max_n == 0) return UT_OK;
+  if (!idx_dev || !out_dev) return set_err(UT_EINVAL, "idx_dev/out_dev is NULL");
+  if (max_n >= (1ull << 31)) return set_err(UT_EINVAL, "max_n must be < 2^31");
+  if (max_n > UINT64_MAX / t->rb) return set_err(UT_EINVAL, "max_n*row_bytes overflows");
+  DevState* s;
+  int rc = dev_state(t, &s);
+  if (rc != UT_OK) return rc;
+  return gather_on(t, s, idx_dev, max_n, out_dev, (cudaStream_t)stream, false, n_dev);
 }
 
 int ut_gather_host(const ut_table* ct, const int64_t* idx_host, uint64_t n, void* out_host,

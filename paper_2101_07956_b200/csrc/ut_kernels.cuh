@@ -161,7 +161,19 @@ struct GatherArgs {
   uint64_t out;     // device address of out byte 0
   unsigned long long* err;
   const uint32_t* perm;   // optional visiting order (work item j handles output row perm[j])
+  const uint64_t* n_dev;  // optional: the row count lives in device memory (min(*n_dev, n))
 };
+
+// The kernels' view of the arguments: n read from device memory when the launch is
+// size-oblivious (ut_gather_dn: a sampler on the device produced the index list).
+__device__ __forceinline__ GatherArgs with_dev_n(const GatherArgs& a) {
+  GatherArgs b = a;
+  if (a.n_dev) {
+    const uint64_t n = *a.n_dev;
+    b.n = n < a.n ? n : a.n;
+  }
+  return b;
+}
 
 // Output row handled by work item j: j itself, or perm[j] when the rows are visited in the
 // translation-locality order built by k_bucket_* (DESIGN.md §Reorder).
@@ -178,7 +190,8 @@ __device__ __forceinline__ void record_bad(unsigned long long* err, uint64_t i) 
 // ---------------------------------------------------------------------------------------------
 // narrow<T>: one thread per row, U rows per thread in flight.
 template <typename T, int U, bool PERM>
-__global__ void __launch_bounds__(256, UT_MINB) k_narrow(GatherArgs a) {
+__global__ void __launch_bounds__(256, UT_MINB) k_narrow(GatherArgs a_) {
+  const GatherArgs a = with_dev_n(a_);
   const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (uint64_t base = 0; base < a.n; base += nthreads * U) {
@@ -209,7 +222,8 @@ __global__ void __launch_bounds__(256, UT_MINB) k_narrow(GatherArgs a) {
 // Single-pass kernels: G lanes per row, 32/G rows per warp step, U steps in flight per warp tile.
 // ALIGNED: base, rb, out 16-B aligned (vec16<G>); else realign<G>.
 template <int G, int U, bool ALIGNED, bool CLIP, bool PERM>
-__global__ void __launch_bounds__(256, UT_MINB) k_single(GatherArgs a) {
+__global__ void __launch_bounds__(256, UT_MINB) k_single(GatherArgs a_) {
+  const GatherArgs a = with_dev_n(a_);
   constexpr int RPS = 32 / G;          // rows per warp step
   constexpr int RPT = RPS * U;         // rows per warp tile
   const int lane = threadIdx.x & 31;
@@ -272,7 +286,8 @@ __global__ void __launch_bounds__(256, UT_MINB) k_single(GatherArgs a) {
 // Multi-pass kernels: one warp per row, the row's source window starts on a 128-B line and is
 // walked 32*U chunks at a time (U LDG.128 per lane in flight).
 template <int U, bool ALIGNED, bool CLIP, bool PERM>
-__global__ void __launch_bounds__(256, UT_MINB) k_multi(GatherArgs a) {
+__global__ void __launch_bounds__(256, UT_MINB) k_multi(GatherArgs a_) {
+  const GatherArgs a = with_dev_n(a_);
   const int lane = threadIdx.x & 31;
   const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -353,7 +368,8 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
 }
 
 template <int U, bool PERM>
-__global__ void __launch_bounds__(256, 1) k_bulk(GatherArgs a) {
+__global__ void __launch_bounds__(256, 1) k_bulk(GatherArgs a_) {
+  const GatherArgs a = with_dev_n(a_);
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[8 * U];
   const int lane = threadIdx.x & 31;
@@ -441,7 +457,8 @@ __global__ void __launch_bounds__(256, 1) k_bulk(GatherArgs a) {
 //                 rotated output position ("the output indices are also identically adjusted").
 // Both need rb % 4 == 0 and 4-B aligned base and out. W = rb / 4.
 template <bool SHIFT>
-__global__ void __launch_bounds__(256) k_paper(GatherArgs a) {
+__global__ void __launch_bounds__(256) k_paper(GatherArgs a_) {
+  const GatherArgs a = with_dev_n(a_);
   const uint64_t W = a.rb >> 2;
   const uint64_t total = a.n * W;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -477,8 +494,9 @@ __device__ __forceinline__ uint32_t bucket_of(const GatherArgs& a, uint64_t i, i
   return (uint64_t)r < a.rows ? (uint32_t)(((uint64_t)r * a.rb) >> shift) : 0u;
 }
 
-__global__ void __launch_bounds__(512) k_bucket_count(GatherArgs a, int shift, uint32_t nb,
+__global__ void __launch_bounds__(512) k_bucket_count(GatherArgs a_, int shift, uint32_t nb,
                                                       uint64_t chunk, uint32_t* cnt) {
+  const GatherArgs a = with_dev_n(a_);
   extern __shared__ uint32_t hist[];    // nb entries
   for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
   __syncthreads();
@@ -520,9 +538,10 @@ __global__ void __launch_bounds__(1024) k_bucket_scan(uint32_t* cnt, uint32_t nb
   for (uint32_t k = threadIdx.x; k < nb; k += 1024) cnt[k] = v[k];
 }
 
-__global__ void __launch_bounds__(512) k_bucket_scatter(GatherArgs a, int shift, uint32_t nb,
+__global__ void __launch_bounds__(512) k_bucket_scatter(GatherArgs a_, int shift, uint32_t nb,
                                                         uint64_t chunk, uint32_t* cursor,
                                                         uint32_t* perm) {
+  const GatherArgs a = with_dev_n(a_);
   extern __shared__ uint32_t hist[];    // nb entries
   for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0u;
   __syncthreads();

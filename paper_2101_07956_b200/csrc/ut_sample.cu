@@ -13,7 +13,9 @@
 // Per hop: k_count (degree, slot count per frontier node) -> exclusive scan -> k_sample (one
 // thread per sample, binary search for its frontier node, one 4-B read of `indices` over the
 // link) -> first-appearance dedup with an epoch-tagged per-node atomicMin table (k_first,
-// k_keep) -> scan of the keep flags -> k_append. Two host syncs per hop read the sizes.
+// k_keep) -> scan of the keep flags -> k_append. Sizes stay in device memory and launches are
+// sized by worst-case bounds, so a call enqueues with no host synchronisation (ut_sample_async,
+// CUDA-graph capturable); ut_sample adds one sync at the end to return the count.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -43,11 +45,15 @@ __device__ __forceinline__ uint64_t sample_hash(uint64_t seed, uint64_t hop, uin
   return mix64(mix64(mix64(seed + (hop + 1) * kPhi) ^ v) + t);
 }
 
-__global__ void k_count(const int64_t* __restrict__ front, uint64_t nf, const int64_t* indptr,
+// All sizes live in device memory (sz[]), so one call enqueues without host synchronisation
+// and can be captured in a CUDA graph; launches are sized by host-side worst-case bounds.
+enum { SZ_NF = 0, SZ_TOTAL = 1, SZ_ADDED = 2, SZ_EPOCH = 3, SZ_N = 4 };
+
+__global__ void k_count(const int64_t* __restrict__ front, const uint64_t* sz, const int64_t* indptr,
                         uint32_t fanout, uint64_t* __restrict__ base, uint64_t* __restrict__ deg,
                         uint32_t* __restrict__ cnt) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nf) return;
+  if (i >= sz[SZ_NF]) return;
   const int64_t v = front[i];
   const int64_t b = indptr[v], e = indptr[v + 1];
   const uint64_t d = (uint64_t)(e - b);
@@ -56,12 +62,13 @@ __global__ void k_count(const int64_t* __restrict__ front, uint64_t nf, const in
   cnt[i] = (uint32_t)(d < fanout ? d : fanout);
 }
 
-__global__ void k_sample(const int64_t* __restrict__ front, uint64_t nf, const uint64_t* __restrict__ base,
-                         const uint64_t* __restrict__ deg, const uint32_t* __restrict__ off,
-                         uint64_t total, uint32_t fanout, uint64_t seed, uint32_t hop,
-                         const int32_t* indices, int64_t* __restrict__ cand) {
+__global__ void k_sample(const int64_t* __restrict__ front, const uint64_t* sz,
+                         const uint64_t* __restrict__ base, const uint64_t* __restrict__ deg,
+                         const uint32_t* __restrict__ off, uint32_t fanout, uint64_t seed,
+                         uint32_t hop, const int32_t* indices, int64_t* __restrict__ cand) {
   const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= total) return;
+  if (j >= sz[SZ_TOTAL]) return;
+  const uint64_t nf = sz[SZ_NF];
   // frontier node of sample j: the last i with off[i] <= j
   uint64_t lo = 0, hi = nf;
   while (hi - lo > 1) {
@@ -80,43 +87,58 @@ __global__ void k_sample(const int64_t* __restrict__ front, uint64_t nf, const u
 }
 
 // First-appearance dedup against the frontier: firstpos[c] keeps the smallest candidate
-// position of node c in this round, tagged with the round's epoch in the high word (a newer
-// round's tag is always smaller, so the table is never cleared).
-__global__ void k_first(const int64_t* __restrict__ cand, uint64_t m, uint64_t n_nodes,
+// position of node c in this round, tagged with the round's epoch (a device counter) in the high
+// word — a newer round's tag is always smaller, so the table is never cleared and graph replays
+// stay correct.
+__device__ __forceinline__ uint64_t round_tag(const uint64_t* sz) {
+  return (uint64_t)(0xFFFFFFFFu - (uint32_t)sz[SZ_EPOCH]) << 32;
+}
+
+__global__ void k_next_round(uint64_t* epoch_dev, uint64_t* sz) {
+  sz[SZ_EPOCH] = ++*epoch_dev;
+}
+
+__global__ void k_first(const int64_t* __restrict__ cand, const uint64_t* sz, uint64_t n_nodes,
                         const uint8_t* __restrict__ in_front, unsigned long long* firstpos,
-                        uint64_t tag_hi, unsigned long long* err) {
+                        unsigned long long* err) {
   const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= m) return;
+  if (j >= sz[SZ_TOTAL]) return;
   const uint64_t c = (uint64_t)cand[j];
   if (c >= n_nodes) {
     atomicMin(err, (unsigned long long)j);
     return;
   }
-  if (!in_front[c]) atomicMin(firstpos + c, (unsigned long long)(tag_hi | j));
+  if (!in_front[c]) atomicMin(firstpos + c, (unsigned long long)(round_tag(sz) | j));
 }
 
-__global__ void k_keep(const int64_t* __restrict__ cand, uint64_t m, uint64_t n_nodes,
+__global__ void k_keep(const int64_t* __restrict__ cand, const uint64_t* sz, uint64_t n_nodes,
                        const uint8_t* __restrict__ in_front, const unsigned long long* __restrict__ firstpos,
-                       uint64_t tag_hi, uint32_t* __restrict__ keep) {
+                       uint32_t* __restrict__ keep) {
   const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= m) return;
+  if (j >= sz[SZ_TOTAL]) return;
   const uint64_t c = (uint64_t)cand[j];
-  keep[j] = (c < n_nodes && !in_front[c] && firstpos[c] == (tag_hi | j)) ? 1u : 0u;
+  keep[j] = (c < n_nodes && !in_front[c] && firstpos[c] == (round_tag(sz) | j)) ? 1u : 0u;
 }
 
-__global__ void k_append(const int64_t* __restrict__ cand, uint64_t m, const uint32_t* __restrict__ keep,
-                         const uint32_t* __restrict__ pos, int64_t* __restrict__ front, uint64_t nf,
-                         uint8_t* __restrict__ in_front) {
+__global__ void k_append(const int64_t* __restrict__ cand, const uint64_t* sz,
+                         const uint32_t* __restrict__ keep, const uint32_t* __restrict__ pos,
+                         int64_t* __restrict__ front, uint8_t* __restrict__ in_front) {
   const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= m || !keep[j]) return;
+  if (j >= sz[SZ_TOTAL] || !keep[j]) return;
   const int64_t c = cand[j];
-  front[nf + pos[j]] = c;
+  front[sz[SZ_NF] + pos[j]] = c;
   in_front[c] = 1;
 }
 
-__global__ void k_clear(const int64_t* __restrict__ front, uint64_t nf, uint8_t* __restrict__ in_front) {
+__global__ void k_grow(uint64_t* sz) { sz[SZ_NF] += sz[SZ_ADDED]; }
+
+__global__ void k_set(uint64_t* sz, int slot, uint64_t v) { sz[slot] = v; }
+
+__global__ void k_finish(const uint64_t* sz, uint64_t* n_out) { *n_out = sz[SZ_NF]; }
+
+__global__ void k_clear(const int64_t* __restrict__ front, const uint64_t* sz, uint8_t* __restrict__ in_front) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < nf) in_front[front[i]] = 0;
+  if (i < sz[SZ_NF]) in_front[front[i]] = 0;
 }
 
 // ---- exclusive scan of uint32 (3 phases: block scans, scan of block sums, add) ---------------
@@ -152,9 +174,11 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* t
   return before + x - v;
 }
 
-__global__ void __launch_bounds__(kScanBlock) k_scan_tiles(const uint32_t* __restrict__ in, uint64_t m,
+// exclusive scan of in[0 .. *m) -> out, grand total -> *total; launched for m_cap elements
+__global__ void __launch_bounds__(kScanBlock) k_scan_tiles(const uint32_t* __restrict__ in, const uint64_t* m_dev,
                                                          uint32_t* __restrict__ out,
                                                          uint32_t* __restrict__ tile_sums) {
+  const uint64_t m = *m_dev;
   const uint64_t t0 = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
   uint32_t v[kScanItems], sum = 0;
 #pragma unroll
@@ -173,8 +197,9 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_tiles(const uint32_t* __res
 }
 
 // One block: exclusive scan of the tile sums in place, grand total to *total.
-__global__ void __launch_bounds__(kScanBlock) k_scan_sums(uint32_t* sums, uint64_t ntiles,
+__global__ void __launch_bounds__(kScanBlock) k_scan_sums(uint32_t* sums, const uint64_t* m_dev,
                                                         uint64_t* total) {
+  const uint64_t ntiles = (*m_dev + kScanTile - 1) / kScanTile;
   uint32_t carry = 0;
   for (uint64_t b0 = 0; b0 < ntiles; b0 += kScanBlock) {
     const uint64_t i = b0 + threadIdx.x;
@@ -187,9 +212,9 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_sums(uint32_t* sums, uint64
   if (threadIdx.x == 0) *total = carry;
 }
 
-__global__ void k_scan_add(uint32_t* out, uint64_t m, const uint32_t* __restrict__ sums) {
+__global__ void k_scan_add(uint32_t* out, const uint64_t* m_dev, const uint32_t* __restrict__ sums) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < m) out[i] += sums[i / kScanTile];
+  if (i < *m_dev && i >= (uint64_t)kScanTile) out[i] += sums[i / kScanTile];
 }
 
 inline int blocks_for(uint64_t n, int per = 256) { return (int)std::max<uint64_t>(1, (n + per - 1) / per); }
@@ -202,6 +227,7 @@ struct ut_graph {
   uint64_t n_nodes = 0, n_edges = 0;
   Pin ip_pin, ix_pin;
   int indptr_hbm = 0;                    // ut_graph_set_option("indptr=hbm")
+  uint64_t launches = 0;                 // kernels enqueued by ut_sample*
   std::mutex mu;
   struct Dev {
     bool init = false;
@@ -210,9 +236,8 @@ struct ut_graph {
     uint8_t* in_front = nullptr;         // n_nodes flags, all zero between calls
     unsigned long long* firstpos = nullptr;   // n_nodes epoch-tagged positions
     unsigned long long* err = nullptr;
-    uint64_t* total_dev = nullptr;       // scan totals
-    uint64_t* total_host = nullptr;      // pinned mirror
-    uint32_t epoch = 0;
+    uint64_t* total_host = nullptr;      // pinned mirror for the synchronous API
+    uint64_t* epoch_dev = nullptr;       // dedup round counter (device, graph-replay safe)
     cudaMemPool_t pool = nullptr;
   } dev[64];
 };
@@ -232,7 +257,7 @@ int graph_dev(ut_graph* g, ut_graph::Dev** out) {
     if ((e = cudaMalloc(&s->in_front, n)) != cudaSuccess ||
         (e = cudaMalloc(&s->firstpos, n * sizeof(unsigned long long))) != cudaSuccess ||
         (e = cudaMalloc(&s->err, sizeof(unsigned long long))) != cudaSuccess ||
-        (e = cudaMalloc(&s->total_dev, 2 * sizeof(uint64_t))) != cudaSuccess ||
+        (e = cudaMalloc(&s->epoch_dev, sizeof(uint64_t))) != cudaSuccess ||
         (e = cudaMallocHost(&s->total_host, 2 * sizeof(uint64_t))) != cudaSuccess) {
       cudaGetLastError();
       return set_err(UT_ENOMEM, "sampler state for %llu nodes", (unsigned long long)n);
@@ -240,6 +265,7 @@ int graph_dev(ut_graph* g, ut_graph::Dev** out) {
     cudaMemset(s->in_front, 0, n);
     cudaMemset(s->firstpos, 0xff, n * sizeof(unsigned long long));
     cudaMemset(s->err, 0xff, sizeof(unsigned long long));
+    cudaMemset(s->epoch_dev, 0, sizeof(uint64_t));
     cudaMemPoolProps props{};
     props.allocType = cudaMemAllocationTypePinned;
     props.location.type = cudaMemLocationTypeDevice;
@@ -263,26 +289,25 @@ int graph_dev(ut_graph* g, ut_graph::Dev** out) {
   return UT_OK;
 }
 
-// exclusive scan of in[0..m) into out, grand total into *total_dev (device)
-cudaError_t scan_u32(const uint32_t* in, uint32_t* out, uint64_t m, uint64_t* total_dev,
-                     uint32_t* tile_sums, cudaStream_t st) {
-  const uint64_t ntiles = (m + kScanTile - 1) / kScanTile;
-  if (m) k_scan_tiles<<<(int)ntiles, kScanBlock, 0, st>>>(in, m, out, tile_sums);
-  k_scan_sums<<<1, kScanBlock, 0, st>>>(tile_sums, ntiles, total_dev);
-  if (m > kScanTile) k_scan_add<<<blocks_for(m), 256, 0, st>>>(out, m, tile_sums);
-  return cudaGetLastError();
+// exclusive scan of in[0 .. *m_dev) into out (launch sized for m_cap), total into *total_dev
+void scan_u32(const uint32_t* in, uint32_t* out, const uint64_t* m_dev, uint64_t m_cap,
+              uint64_t* total_dev, uint32_t* tile_sums, cudaStream_t st) {
+  const uint64_t ntiles = std::max<uint64_t>(1, (m_cap + kScanTile - 1) / kScanTile);
+  k_scan_tiles<<<(int)ntiles, kScanBlock, 0, st>>>(in, m_dev, out, tile_sums);
+  k_scan_sums<<<1, kScanBlock, 0, st>>>(tile_sums, m_dev, total_dev);
+  if (m_cap > kScanTile) k_scan_add<<<blocks_for(m_cap), 256, 0, st>>>(out, m_dev, tile_sums);
 }
 
-int read_total(ut_graph::Dev* s, cudaStream_t st, uint64_t* v) {
-  cudaError_t e = cudaMemcpyAsync(s->total_host, s->total_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (e != cudaSuccess) return cuda_err(e, "sampler size read-back");
-  *v = s->total_host[0];
-  return UT_OK;
+// Worst-case frontier sizes: every hop adds at most fanout new nodes per frontier node.
+uint64_t frontier_cap(uint64_t n_seeds, const int32_t* fanouts, int hops, uint64_t n_nodes, int upto) {
+  uint64_t c = n_seeds;
+  for (int h = 0; h < upto && h < hops; ++h) c = std::min<uint64_t>(n_nodes, c + c * (uint64_t)fanouts[h]);
+  return std::max<uint64_t>(c, 1);
 }
 
 template <typename T>
 int pool_alloc(ut_graph::Dev* s, T** p, uint64_t count, cudaStream_t st) {
+  *p = nullptr;
   cudaError_t e = cudaMallocFromPoolAsync((void**)p, std::max<uint64_t>(1, count) * sizeof(T), s->pool, st);
   if (e != cudaSuccess) return cuda_err(e, "cudaMallocFromPoolAsync(sampler)");
   return UT_OK;
@@ -333,7 +358,7 @@ int ut_graph_release(ut_graph* g) {
     cudaFree(s.in_front);
     cudaFree(s.firstpos);
     cudaFree(s.err);
-    cudaFree(s.total_dev);
+    cudaFree(s.epoch_dev);
     cudaFreeHost(s.total_host);
     cudaFree(s.indptr_copy);
     if (s.pool) cudaMemPoolDestroy(s.pool);
@@ -345,6 +370,8 @@ int ut_graph_release(ut_graph* g) {
   return UT_OK;
 }
 
+uint64_t ut_graph_launches(const ut_graph* g) { return g ? g->launches : 0; }
+
 int ut_graph_set_option(ut_graph* g, const char* opt) {
   if (!g || !opt) return set_err(UT_EINVAL, "NULL argument");
   if (!strcmp(opt, "indptr=hbm")) g->indptr_hbm = 1;
@@ -353,116 +380,157 @@ int ut_graph_set_option(ut_graph* g, const char* opt) {
   return UT_OK;
 }
 
-int ut_sample(ut_graph* g, const int64_t* seeds_dev, uint64_t n_seeds, const int32_t* fanouts,
-              int n_hops, uint64_t seed, int64_t* nodes_dev, uint64_t cap, uint64_t* n_out,
-              ut_stream_t stream) {
-  if (!g || !n_out || (n_seeds && !seeds_dev) || (n_hops > 0 && !fanouts) || n_hops < 0)
+}  // extern "C"
+
+namespace {
+
+// Enqueue the whole sampler on `st`: no host synchronisation, launches sized by the worst case.
+// `front` (capacity >= frontier_cap(all hops)) receives the node list, *n_dev its length.
+int sample_enqueue(ut_graph* g, ut_graph::Dev* s, const int64_t* seeds_dev, uint64_t n_seeds,
+                   const int32_t* fanouts, int n_hops, uint64_t seed, int64_t* front,
+                   uint64_t* n_dev, cudaStream_t st) {
+  const int64_t* indptr = g->indptr_hbm ? s->indptr_copy : (const int64_t*)s->indptr_dev;
+  const int32_t* indices = (const int32_t*)s->indices_dev;
+  uint64_t max_m = n_seeds;
+  for (int h = 0; h < n_hops; ++h)
+    max_m = std::max<uint64_t>(max_m, frontier_cap(n_seeds, fanouts, n_hops, g->n_nodes, h) * (uint64_t)fanouts[h]);
+  const uint64_t fcap = frontier_cap(n_seeds, fanouts, n_hops, g->n_nodes, n_hops);
+  if (max_m >= (1ull << 32) || fcap >= (1ull << 32)) return set_err(UT_EINVAL, "sampling bound exceeds 2^32");
+  uint64_t* sz = nullptr;
+  uint64_t *base = nullptr, *deg = nullptr;
+  uint32_t *cnt = nullptr, *off = nullptr, *keep = nullptr, *pos = nullptr, *sums = nullptr;
+  int64_t* cand = nullptr;
+  int rc;
+  if ((rc = pool_alloc(s, &sz, SZ_N, st)) != UT_OK || (rc = pool_alloc(s, &base, fcap, st)) != UT_OK ||
+      (rc = pool_alloc(s, &deg, fcap, st)) != UT_OK || (rc = pool_alloc(s, &cnt, fcap, st)) != UT_OK ||
+      (rc = pool_alloc(s, &off, fcap, st)) != UT_OK || (rc = pool_alloc(s, &keep, max_m, st)) != UT_OK ||
+      (rc = pool_alloc(s, &pos, max_m, st)) != UT_OK ||
+      (rc = pool_alloc(s, &sums, std::max(max_m, fcap) / kScanTile + 2, st)) != UT_OK ||
+      (rc = pool_alloc(s, &cand, max_m, st)) != UT_OK)
+    return rc;
+  k_set<<<1, 1, 0, st>>>(sz, SZ_NF, 0);
+  // merge `m_cap`-bounded candidates (count in sz[SZ_TOTAL]) into the frontier
+  auto merge = [&](const int64_t* c, uint64_t m_cap) {
+    k_next_round<<<1, 1, 0, st>>>(s->epoch_dev, sz);
+    k_first<<<blocks_for(m_cap), 256, 0, st>>>(c, sz, g->n_nodes, s->in_front, s->firstpos, s->err);
+    k_keep<<<blocks_for(m_cap), 256, 0, st>>>(c, sz, g->n_nodes, s->in_front, s->firstpos, keep);
+    scan_u32(keep, pos, sz + SZ_TOTAL, m_cap, sz + SZ_ADDED, sums, st);
+    k_append<<<blocks_for(m_cap), 256, 0, st>>>(c, sz, keep, pos, front, s->in_front);
+    k_grow<<<1, 1, 0, st>>>(sz);
+  };
+  k_set<<<1, 1, 0, st>>>(sz, SZ_TOTAL, n_seeds);
+  merge(seeds_dev, n_seeds);
+  for (int h = 0; h < n_hops; ++h) {
+    const uint32_t f = (uint32_t)fanouts[h];
+    if (f == 0) continue;
+    const uint64_t nf_cap = frontier_cap(n_seeds, fanouts, n_hops, g->n_nodes, h);
+    const uint64_t m_cap = nf_cap * f;
+    k_count<<<blocks_for(nf_cap), 256, 0, st>>>(front, sz, indptr, f, base, deg, cnt);
+    scan_u32(cnt, off, sz + SZ_NF, nf_cap, sz + SZ_TOTAL, sums, st);
+    k_sample<<<blocks_for(m_cap), 256, 0, st>>>(front, sz, base, deg, off, f, seed, (uint32_t)h,
+                                                indices, cand);
+    merge(cand, m_cap);
+  }
+  k_finish<<<1, 1, 0, st>>>(sz, n_dev);
+  k_clear<<<blocks_for(fcap), 256, 0, st>>>(front, sz, s->in_front);
+  // kernels: 2 k_set + merge (k_next_round, k_first, k_keep, 2-3 scan, k_append, k_grow) per
+  // merge + (k_count, 2-3 scan, k_sample) per hop + k_finish + k_clear
+  auto scan_k = [](uint64_t m) { return m > (uint64_t)kScanTile ? 3u : 2u; };
+  uint64_t k = 2 + 2 + (5 + scan_k(n_seeds));
+  for (int h = 0; h < n_hops; ++h) {
+    if (!fanouts[h]) continue;
+    const uint64_t nf_cap = frontier_cap(n_seeds, fanouts, n_hops, g->n_nodes, h);
+    k += 2 + scan_k(nf_cap) + 5 + scan_k(nf_cap * (uint64_t)fanouts[h]);
+  }
+  g->launches += k;
+  for (void* p : {(void*)sz, (void*)base, (void*)deg, (void*)cnt, (void*)off, (void*)keep,
+                  (void*)pos, (void*)sums, (void*)cand})
+    cudaFreeAsync(p, st);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_err(e, "sampler launch");
+  return UT_OK;
+}
+
+int check_sample_args(ut_graph* g, const int64_t* seeds_dev, uint64_t n_seeds, const int32_t* fanouts,
+                      int n_hops) {
+  if (!g || (n_seeds && !seeds_dev) || (n_hops > 0 && !fanouts) || n_hops < 0)
     return set_err(UT_EINVAL, "NULL or negative argument");
   for (int h = 0; h < n_hops; ++h)
     if (fanouts[h] < 0) return set_err(UT_EINVAL, "fanout %d is negative", h);
+  return UT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t ut_sample_capacity(uint64_t n_seeds, const int32_t* fanouts, int n_hops, uint64_t n_nodes) {
+  if (n_seeds == 0 || (n_hops > 0 && !fanouts)) return n_seeds;
+  return frontier_cap(n_seeds, fanouts, n_hops, n_nodes ? n_nodes : UINT64_MAX, n_hops);
+}
+
+int ut_sample_async(ut_graph* g, const int64_t* seeds_dev, uint64_t n_seeds, const int32_t* fanouts,
+                    int n_hops, uint64_t seed, int64_t* nodes_dev, uint64_t cap, uint64_t* n_out_dev,
+                    ut_stream_t stream) {
+  int rc = check_sample_args(g, seeds_dev, n_seeds, fanouts, n_hops);
+  if (rc != UT_OK) return rc;
+  if (!n_out_dev || !nodes_dev) return set_err(UT_EINVAL, "NULL nodes_dev / n_out_dev");
+  const uint64_t need = ut_sample_capacity(n_seeds, fanouts, n_hops, g->n_nodes);
+  if (cap < need) return set_err(UT_EINVAL, "nodes capacity %llu < worst case %llu",
+                                 (unsigned long long)cap, (unsigned long long)need);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n_seeds == 0) {
+    k_set<<<1, 1, 0, st>>>(n_out_dev, 0, 0);
+    return UT_OK;
+  }
+  std::lock_guard<std::mutex> lk(g->mu);
+  ut_graph::Dev* s;
+  if ((rc = graph_dev(g, &s)) != UT_OK) return rc;
+  return sample_enqueue(g, s, seeds_dev, n_seeds, fanouts, n_hops, seed, nodes_dev, n_out_dev, st);
+}
+
+int ut_sample(ut_graph* g, const int64_t* seeds_dev, uint64_t n_seeds, const int32_t* fanouts,
+              int n_hops, uint64_t seed, int64_t* nodes_dev, uint64_t cap, uint64_t* n_out,
+              ut_stream_t stream) {
+  int rc = check_sample_args(g, seeds_dev, n_seeds, fanouts, n_hops);
+  if (rc != UT_OK) return rc;
+  if (!n_out) return set_err(UT_EINVAL, "NULL n_out");
   *n_out = 0;
   if (n_seeds == 0) return UT_OK;
   std::lock_guard<std::mutex> lk(g->mu);
   ut_graph::Dev* s;
-  int rc = graph_dev(g, &s);
-  if (rc != UT_OK) return rc;
+  if ((rc = graph_dev(g, &s)) != UT_OK) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  const int64_t* indptr = g->indptr_hbm ? s->indptr_copy : (const int64_t*)s->indptr_dev;
-  const int32_t* indices = (const int32_t*)s->indices_dev;
-
-  // capacity of the frontier: every hop can add at most fanout new nodes per frontier node
-  uint64_t fcap = n_seeds;
-  for (int h = 0; h < n_hops; ++h) {
-    fcap = std::min<uint64_t>(g->n_nodes, fcap + fcap * (uint64_t)fanouts[h]);
-  }
-  fcap = std::max<uint64_t>(fcap, n_seeds);
-  int64_t* front = nullptr;
-  if ((rc = pool_alloc(s, &front, fcap, st)) != UT_OK) return rc;
-  uint64_t nf = 0;
-  int status = UT_OK;
+  const uint64_t fcap = ut_sample_capacity(n_seeds, fanouts, n_hops, g->n_nodes);
+  int64_t* front = nodes_dev;
+  const bool own = cap < fcap || !nodes_dev;
+  uint64_t* n_dev = nullptr;
+  if ((rc = pool_alloc(s, &n_dev, 1, st)) != UT_OK) return rc;
+  if (own && (rc = pool_alloc(s, &front, fcap, st)) != UT_OK) return rc;
+  rc = sample_enqueue(g, s, seeds_dev, n_seeds, fanouts, n_hops, seed, front, n_dev, st);
   cudaError_t e = cudaSuccess;
-
-  // merge `m` candidates into the frontier (first appearance, not yet present)
-  auto merge = [&](const int64_t* cand, uint64_t m) -> int {
-    if (m == 0) return UT_OK;
-    if (++s->epoch == 0xFFFFFFFFu) {   // tags exhausted: reset the table once per 4G rounds
-      cudaMemsetAsync(s->firstpos, 0xff, g->n_nodes * sizeof(unsigned long long), st);
-      s->epoch = 1;
-    }
-    const uint64_t tag_hi = (uint64_t)(0xFFFFFFFFu - s->epoch) << 32;
-    uint32_t *keep = nullptr, *pos = nullptr, *sums = nullptr;
-    int r;
-    if ((r = pool_alloc(s, &keep, m, st)) != UT_OK || (r = pool_alloc(s, &pos, m, st)) != UT_OK ||
-        (r = pool_alloc(s, &sums, m / kScanTile + 1, st)) != UT_OK)
-      return r;
-    k_first<<<blocks_for(m), 256, 0, st>>>(cand, m, g->n_nodes, s->in_front, s->firstpos, tag_hi, s->err);
-    k_keep<<<blocks_for(m), 256, 0, st>>>(cand, m, g->n_nodes, s->in_front, s->firstpos, tag_hi, keep);
-    if ((e = scan_u32(keep, pos, m, s->total_dev, sums, st)) != cudaSuccess) return cuda_err(e, "scan");
-    k_append<<<blocks_for(m), 256, 0, st>>>(cand, m, keep, pos, front, nf, s->in_front);
-    uint64_t added = 0;
-    if ((r = read_total(s, st, &added)) != UT_OK) return r;
-    nf += added;
-    cudaFreeAsync(keep, st);
-    cudaFreeAsync(pos, st);
-    cudaFreeAsync(sums, st);
-    return UT_OK;
-  };
-
-  status = merge(seeds_dev, n_seeds);
-  unsigned long long bad = ~0ull;
-  if (status == UT_OK) {
+  if (rc == UT_OK) {
+    cudaMemcpyAsync(&s->total_host[0], n_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(&s->total_host[1], s->err, sizeof(uint64_t), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    bad = s->total_host[1];
-    if (bad != ~0ull) {
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) rc = cuda_err(e, "sampler");
+  }
+  if (rc == UT_OK) {
+    const uint64_t n = s->total_host[0];
+    *n_out = n;
+    if (s->total_host[1] != ~0ull) {
       cudaMemsetAsync(s->err, 0xff, sizeof(unsigned long long), st);
-      status = set_err(UT_ERANGE, "seed %llu is out of range", bad);
+      rc = set_err(UT_ERANGE, "seed %llu is out of range", (unsigned long long)s->total_host[1]);
+    } else if (own) {
+      if (n > cap || !nodes_dev)
+        rc = set_err(UT_EINVAL, "nodes buffer holds %llu, need %llu", (unsigned long long)cap,
+                     (unsigned long long)n);
+      else if ((e = cudaMemcpyAsync(nodes_dev, front, n * sizeof(int64_t), cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+        rc = cuda_err(e, "copy nodes");
     }
   }
-  for (int h = 0; h < n_hops && status == UT_OK; ++h) {
-    const uint32_t f = (uint32_t)fanouts[h];
-    if (f == 0 || nf == 0) continue;
-    uint64_t *base = nullptr, *deg = nullptr;
-    uint32_t *cnt = nullptr, *off = nullptr, *sums = nullptr;
-    int64_t* cand = nullptr;
-    if ((status = pool_alloc(s, &base, nf, st)) != UT_OK || (status = pool_alloc(s, &deg, nf, st)) != UT_OK ||
-        (status = pool_alloc(s, &cnt, nf, st)) != UT_OK || (status = pool_alloc(s, &off, nf, st)) != UT_OK ||
-        (status = pool_alloc(s, &sums, nf / kScanTile + 1, st)) != UT_OK)
-      break;
-    k_count<<<blocks_for(nf), 256, 0, st>>>(front, nf, indptr, f, base, deg, cnt);
-    if ((e = scan_u32(cnt, off, nf, s->total_dev, sums, st)) != cudaSuccess) {
-      status = cuda_err(e, "scan");
-      break;
-    }
-    uint64_t total = 0;
-    if ((status = read_total(s, st, &total)) != UT_OK) break;
-    if ((status = pool_alloc(s, &cand, total, st)) != UT_OK) break;
-    if (total)
-      k_sample<<<blocks_for(total), 256, 0, st>>>(front, nf, base, deg, off, total, f, seed,
-                                                  (uint32_t)h, indices, cand);
-    if ((e = cudaGetLastError()) != cudaSuccess) {
-      status = cuda_err(e, "k_sample");
-      break;
-    }
-    status = merge(cand, total);
-    cudaFreeAsync(base, st);
-    cudaFreeAsync(deg, st);
-    cudaFreeAsync(cnt, st);
-    cudaFreeAsync(off, st);
-    cudaFreeAsync(sums, st);
-    cudaFreeAsync(cand, st);
-  }
-  if (status == UT_OK) {
-    *n_out = nf;
-    if (nf > cap || !nodes_dev) status = set_err(UT_EINVAL, "nodes buffer holds %llu, need %llu",
-                                                 (unsigned long long)cap, (unsigned long long)nf);
-    else if ((e = cudaMemcpyAsync(nodes_dev, front, nf * sizeof(int64_t), cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
-      status = cuda_err(e, "copy nodes");
-  }
-  if (nf) k_clear<<<blocks_for(nf), 256, 0, st>>>(front, nf, s->in_front);
-  cudaFreeAsync(front, st);
-  if ((e = cudaGetLastError()) != cudaSuccess && status == UT_OK) status = cuda_err(e, "sampler");
-  return status;
+  if (own) cudaFreeAsync(front, st);
+  cudaFreeAsync(n_dev, st);
+  return rc;
 }
 
 }  // extern "C"

@@ -128,3 +128,71 @@ def test_errors_and_edge_cases():
     with pytest.raises(ut.UTError):
         bad = np.array([0, 5, 3], dtype=np.int64)      # indptr[n] != n_edges
         ut.Graph(bad.ctypes.data, c.indices.ctypes.data, 2, 2)
+
+
+def test_async_sample_gather_dn_and_cuda_graph(products_csr):
+    """ut_sample_async + ut_gather_dn: no host sync between sampling and gathering; the whole
+    minibatch captured once in a CUDA graph and replayed for new seeds matches the oracle."""
+    c = products_csr
+    rows, rb = c.n_nodes, 400
+    hb = workloads.HostBuffer(rows * rb)
+    workloads.fill_table(hb.addr, rows, rb, 6, threads=0)
+    fan = [15, 10, 5]
+    rng = np.random.default_rng(3)
+    with ut.Graph(c.indptr_addr, c.indices_addr, c.n_nodes, c.n_edges, keep=c) as g, \
+            ut.Table(hb.addr, rows, rb) as t:
+        cap = g.capacity(1024, fan)
+        assert cap == min(rows, 1024 * 16 * 11 * 6)
+        seeds = torch.empty(1024, dtype=torch.int64, device="cuda")
+        nodes = torch.empty(cap, dtype=torch.int64, device="cuda")
+        n_dev = torch.zeros(1, dtype=torch.int64, device="cuda")
+        out = torch.empty(cap * rb, dtype=torch.uint8, device="cuda")
+
+        def check(seed_np, salt):
+            want_nodes = oracle.sample(c.indptr_addr, c.indices_addr, rows, seed_np, fan, salt)
+            n = int(n_dev.item())
+            assert n == want_nodes.size
+            np.testing.assert_array_equal(nodes[:n].cpu().numpy(), want_nodes)
+            want, _ = oracle.gather(hb.addr, rows, rb, want_nodes)
+            assert out[: n * rb].cpu().numpy().tobytes() == want.tobytes()
+
+        # eager, asynchronous
+        s0 = rng.choice(rows, size=1024, replace=False)
+        seeds.copy_(torch.from_numpy(s0))
+        g.sample_async(seeds, fan, 21, nodes, n_dev)
+        t.gather_dn(nodes, n_dev, out)
+        torch.cuda.synchronize()
+        check(s0, 21)
+        # captured once, replayed with new seeds in the same buffer
+        stream = torch.cuda.Stream()
+        graph = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=stream):
+            g.sample_async(seeds, fan, 22, nodes, n_dev, stream=stream)
+            t.gather_dn(nodes, n_dev, out, stream=stream)
+        for _ in range(3):
+            s1 = rng.choice(rows, size=1024, replace=False)
+            seeds.copy_(torch.from_numpy(s1))
+            torch.cuda.synchronize()
+            graph.replay()
+            torch.cuda.synchronize()
+            check(s1, 22)
+    hb.close()
+
+
+def test_gather_dn_counts_on_device():
+    rows, rb = 5000, 68
+    hb = workloads.HostBuffer(rows * rb, offset=5)
+    workloads.fill_table(hb.addr, rows, rb, 8)
+    idx = workloads.uniform_idx(3000, rows, 9)
+    with ut.Table(hb.addr, rows, rb) as t:
+        for n, reorder in [(0, "off"), (1, "off"), (1777, "off"), (3000, "on"), (5000, "on")]:
+            t.set_plan(f"reorder={reorder}")
+            out = torch.full((3000 * rb,), 0xAB, dtype=torch.uint8, device="cuda")
+            t.gather_dn(torch.from_numpy(idx).cuda(), torch.tensor([n], device="cuda"), out)
+            m = min(n, 3000)
+            want, _ = oracle.gather(hb.addr, rows, rb, idx[:m])
+            got = out.cpu().numpy()
+            assert got[: m * rb].tobytes() == want.tobytes()
+            assert (got[m * rb:] == 0xAB).all()
+    hb.close()
