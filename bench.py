@@ -548,7 +548,8 @@ class GpuSampling:
         self.csr = workloads.CSRGraph(spec["rows"], spec["edges"], seed=seed, threads=0)
         self.graph = ut.Graph(self.csr.indptr_addr, self.csr.indices_addr, self.csr.n_nodes,
                               self.csr.n_edges, keep=self.csr)
-        self.graph.set_option(f"indptr={indptr}")
+        for opt in indptr.split(","):
+            self.graph.set_option(f"indptr={opt}" if opt in ("host", "hbm") else opt)
         self.indptr = indptr
         perm = np.random.default_rng(seed + 99).permutation(spec["rows"])
         B = spec["batch"]
@@ -765,8 +766,8 @@ def main(argv=None):
     ap.add_argument("--sample", default="cpu", choices=["cpu", "gpu"],
                     help="cpu: index lists sampled before timing (default, the paper's split); "
                          "gpu: ut_sample inside every timed step (SURVEY NEXT-2)")
-    ap.add_argument("--graph-indptr", default="host", choices=["host", "hbm"],
-                    help="with --sample gpu: CSR indptr read over the link or copied to HBM")
+    ap.add_argument("--graph-indptr", default="host",
+                    help="with --sample gpu: 'host' or 'hbm' for indptr, optionally ',indices=hbm'")
     ap.add_argument("--async-sample", action="store_true",
                     help="with --sample gpu: ut_sample_async + ut_gather_dn (no host sync)")
     ap.add_argument("--graph", action="store_true",

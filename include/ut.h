@@ -230,7 +230,8 @@ UT_API ut_graph* ut_graph_register(const int64_t* indptr, const int32_t* indices
                                    uint64_t n_edges);
 
 /* "indptr=hbm" keeps a device copy of indptr (8*(n_nodes+1) bytes) so only `indices` is read
- * over the link; "indptr=host" (default) reads both over the link. */
+ * over the link; "indices=hbm" keeps a device copy of indices (4*n_edges bytes); "...=host"
+ * (the default for both) reads that array over the link. */
 UT_API int ut_graph_set_option(ut_graph* g, const char* option);
 
 /*

@@ -227,12 +227,14 @@ struct ut_graph {
   uint64_t n_nodes = 0, n_edges = 0;
   Pin ip_pin, ix_pin;
   int indptr_hbm = 0;                    // ut_graph_set_option("indptr=hbm")
+  int indices_hbm = 0;                   // ut_graph_set_option("indices=hbm")
   uint64_t launches = 0;                 // kernels enqueued by ut_sample*
   std::mutex mu;
   struct Dev {
     bool init = false;
     uint64_t indptr_dev = 0, indices_dev = 0;
     int64_t* indptr_copy = nullptr;      // HBM copy when indptr_hbm
+    int32_t* indices_copy = nullptr;     // HBM copy when indices_hbm
     uint8_t* in_front = nullptr;         // n_nodes flags, all zero between calls
     unsigned long long* firstpos = nullptr;   // n_nodes epoch-tagged positions
     unsigned long long* err = nullptr;
@@ -284,6 +286,15 @@ int graph_dev(ut_graph* g, ut_graph::Dev** out) {
     }
     if ((e = cudaMemcpy(s->indptr_copy, g->indptr, bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
       return cuda_err(e, "indptr H2D");
+  }
+  if (g->indices_hbm && !s->indices_copy) {
+    const uint64_t bytes = std::max<uint64_t>(1, g->n_edges) * sizeof(int32_t);
+    if ((e = cudaMalloc(&s->indices_copy, bytes)) != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(UT_ENOMEM, "HBM copy of indices (%llu bytes)", (unsigned long long)bytes);
+    }
+    if ((e = cudaMemcpy(s->indices_copy, g->indices, bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
+      return cuda_err(e, "indices H2D");
   }
   *out = s;
   return UT_OK;
@@ -352,7 +363,7 @@ int ut_graph_release(ut_graph* g) {
   cudaGetDevice(&cur);
   for (int d = 0; d < 64; ++d) {
     ut_graph::Dev& s = g->dev[d];
-    if (!s.init && !s.indptr_copy) continue;
+    if (!s.init && !s.indptr_copy && !s.indices_copy) continue;
     cudaSetDevice(d);
     cudaDeviceSynchronize();
     cudaFree(s.in_front);
@@ -361,6 +372,7 @@ int ut_graph_release(ut_graph* g) {
     cudaFree(s.epoch_dev);
     cudaFreeHost(s.total_host);
     cudaFree(s.indptr_copy);
+    cudaFree(s.indices_copy);
     if (s.pool) cudaMemPoolDestroy(s.pool);
   }
   cudaSetDevice(cur);
@@ -376,6 +388,8 @@ int ut_graph_set_option(ut_graph* g, const char* opt) {
   if (!g || !opt) return set_err(UT_EINVAL, "NULL argument");
   if (!strcmp(opt, "indptr=hbm")) g->indptr_hbm = 1;
   else if (!strcmp(opt, "indptr=host")) g->indptr_hbm = 0;
+  else if (!strcmp(opt, "indices=hbm")) g->indices_hbm = 1;
+  else if (!strcmp(opt, "indices=host")) g->indices_hbm = 0;
   else return set_err(UT_EINVAL, "unknown option '%s'", opt);
   return UT_OK;
 }
@@ -390,7 +404,7 @@ int sample_enqueue(ut_graph* g, ut_graph::Dev* s, const int64_t* seeds_dev, uint
                    const int32_t* fanouts, int n_hops, uint64_t seed, int64_t* front,
                    uint64_t* n_dev, cudaStream_t st) {
   const int64_t* indptr = g->indptr_hbm ? s->indptr_copy : (const int64_t*)s->indptr_dev;
-  const int32_t* indices = (const int32_t*)s->indices_dev;
+  const int32_t* indices = g->indices_hbm ? s->indices_copy : (const int32_t*)s->indices_dev;
   uint64_t max_m = n_seeds;
   for (int h = 0; h < n_hops; ++h)
     max_m = std::max<uint64_t>(max_m, frontier_cap(n_seeds, fanouts, n_hops, g->n_nodes, h) * (uint64_t)fanouts[h]);

@@ -76,7 +76,7 @@ def products_csr():
     g.close()
 
 
-@pytest.mark.parametrize("opt", ["indptr=host", "indptr=hbm"])
+@pytest.mark.parametrize("opt", ["indptr=host", "indptr=hbm", "indices=hbm"])
 def test_products_shaped_minibatches(products_csr, opt):
     c = products_csr
     with ut.Graph(c.indptr_addr, c.indices_addr, c.n_nodes, c.n_edges, keep=c) as g:
