@@ -195,7 +195,8 @@ UT_API const char* ut_plan_probe(uint64_t base, uint64_t rows, uint64_t row_byte
  * for reordered gathers from tables > 1 GiB.
  * "reorder=on|off|auto" controls the translation-locality stage instead:
  * work items are visited grouped by the 2-MiB table region their row lies in, the output order
- * is unchanged; "auto" enables it for tables > 1 GiB and gathers of >= 4 MiB.
+ * is unchanged; "auto" enables it for gathers of >= 64K rows narrower than 4 KiB from tables
+ * > 1 GiB (or > 64 MiB for rows <= 128 B; not for managed tables unless rows <= 128 B).
  * The environment variables UT_PLAN and UT_REORDER, read at ut_register, do the same.
  */
 UT_API int ut_set_plan(ut_table* t, const char* name);

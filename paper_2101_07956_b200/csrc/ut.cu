@@ -605,7 +605,10 @@ Shape shape_for(const ut_table* t, const DevState* s, bool reordered, uint64_t n
 bool want_reorder(const ut_table* t, uint64_t n) {
   if (t->reorder == 0) return false;
   if (t->reorder == 1) return true;
-  if (n < 4096 || n * t->rb < (4ull << 20)) return false;
+  // the stage costs ~30 us; it pays from ~64K rows (Fig. 7 replica: 8K-32K rows of 1 KB over a
+  // 4-GiB pool lose 5-15 % with it, 128K+ gain), and rows >= 4 KB span enough lines per
+  // translation that order does not matter (profiles/r1_fig7_replica*.jsonl)
+  if (n < 65536 || t->rb >= 4096) return false;
   // beyond the ~1-GiB translation reach of registered / pinned memory every row size gains;
   // below it — and on managed tables, whose mappings have no such reach limit on this box —
   // only small rows, whose request rate (not bytes) is the limit, gain from visiting
