@@ -470,6 +470,26 @@ def run_ut(args, spec, dist):
         e2e = {"value": round(e_tot / mx / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps),
                "path": "ut_gather_host: idx H2D copy, then the gather kernel stores rows into pinned host memory"}
+        # the paper's own pipeline (Listing 2): CPU-sampled index list -> GPU rows for training;
+        # pinned idx H2D, gather into HBM, then an 8-byte read-back of the step's result
+        f_sec, f_bytes = 0.0, 0
+        probe = torch.empty(1, dtype=torch.int64, pin_memory=True)
+        for s in range(args.steps):
+            ih = idx_host[(args.warmup + s) % count]
+            flush.zero_()
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            idx_d = ih.to("cuda", non_blocking=True)
+            res = table.gather(idx_d, out=out[: ih.numel() * rb])
+            probe.copy_(res[:8].view(torch.int64), non_blocking=False)
+            f_sec += time.perf_counter() - t1
+            f_bytes += ih.numel() * rb
+        mx = dist.allreduce([f_sec], "max")[0]
+        f_tot = dist.allreduce([float(f_bytes)], "sum")[0]
+        e2e["to_hbm"] = {"value": round(f_tot / mx / 1e9, 3), "unit": "GB/s",
+                         "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": 8,
+                         "path": "Table.gather with a pinned host idx: idx H2D, gather into HBM, "
+                                 "8-B read-back of the result (the paper's Listing 2 pipeline)"}
         del out_host, idx_host
 
     # optional NCCL all-reduce smoke step (SURVEY §2.3 ii): off the gather path, untimed
