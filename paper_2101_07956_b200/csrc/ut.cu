@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <unordered_map>
 #include <vector>
 #include <cstdarg>
 #include <cstdio>
@@ -337,11 +338,24 @@ int blocks_per_sm_cap() {
   return cap;
 }
 
-template <typename K>
-int grid_for(K kernel, int sms, uint64_t work_warps, int cap_blocks = 0) {
+// Resident 256-thread blocks per SM of a kernel, queried once per kernel (the occupancy query
+// costs microseconds of host time per call otherwise).
+int occupancy(const void* kernel) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(kernel);
+  if (it != cache.end()) return it->second;
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
   if (per_sm <= 0) per_sm = 1;
+  cache[kernel] = per_sm;
+  return per_sm;
+}
+
+template <typename K>
+int grid_for(K kernel, int sms, uint64_t work_warps, int cap_blocks = 0) {
+  int per_sm = occupancy((const void*)kernel);
   if (blocks_per_sm_cap() > 0) per_sm = std::min(per_sm, blocks_per_sm_cap());
   else if (blocks_per_sm_cap() < 0 && cap_blocks < 0) per_sm = std::min(per_sm, -cap_blocks);
   uint64_t full = (uint64_t)sms * per_sm;
