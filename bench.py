@@ -224,6 +224,28 @@ def h2d_ceiling(torch, nbytes: int = 1 << 30, reps: int = 10) -> float:
     return best
 
 
+def sm_read_ceiling(torch, ut, nbytes: int = 1 << 30, reps: int = 5) -> float:
+    """The SM-issued sysmem read ceiling (GB/s): this library's own kernel gathering 512-B rows
+    in order from a 1-GiB pinned buffer (whole 128-B lines, sequential addresses) — the most a
+    load-based gather can pull over the link, next to the copy engine's memcpy ceiling."""
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    rows = nbytes // 512
+    idx = torch.arange(rows, dtype=torch.int64, device="cuda")
+    out = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    best = 0.0
+    with ut.Table(h.data_ptr(), rows, 512) as t:
+        for _ in range(reps + 1):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            t.gather(idx, out=out)
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, nbytes / e0.elapsed_time(e1) / 1e6)
+    del h, out, idx
+    return best
+
+
 def cpu_oracle_rate(table_addr: int, spec: dict, lists: list[np.ndarray], budget_s: float):
     """The oracle as it stands, on this host, over a bounded sample of the same index lists."""
     import oracle
@@ -369,6 +391,7 @@ def run_ut(args, spec, dist):
     dist.barrier()
     link = h2d_ceiling(torch)
     link_sum = dist.allreduce([link], "sum")[0]
+    sm_ceiling = sm_read_ceiling(torch, ut)
 
     # parity (outside timing): the first minibatch against the oracle, byte for byte
     parity = None
@@ -531,6 +554,8 @@ def run_ut(args, spec, dist):
             "host_dram_read_gbs": dram,
             "box_roofline_gbs": round(min(link_sum, dram), 3) if dram else round(link_sum, 3),
             "frac_of_link": round(per_gpu / link, 4),
+            "sm_read_ceiling_gbs": round(sm_ceiling, 3),
+            "frac_of_sm_read_ceiling": round(per_gpu / sm_ceiling, 4),
             "plan": table.plan, "table_memory": args.alloc,
             "roofline": {"bound": "pcie_h2d",
                          "achieved": round(achieved, 3) if achieved is not None else None,
@@ -538,7 +563,8 @@ def run_ut(args, spec, dist):
                          "frac": round(achieved / link, 4) if achieved is not None else None,
                          "traffic": None,
                          "kernel": f"gather {table.plan} (device time of the gather kernel alone, CUDA events on its stream)",
-                         "peak_source": "pinned cudaMemcpy H2D measured in this run (best of 10 x 1 GiB)"},
+                         "peak_source": "pinned cudaMemcpy H2D measured in this run (best of 10 x 1 GiB)",
+                         "sm_read_ceiling": round(sm_ceiling, 3)},
             "cpu_baseline": cpu_base, "py_baseline": py_base, "e2e": e2e,
             "gpu_launches": n_launch, "clocks": clk,
             "sampling": sampler.report(args.steps) if sampler is not None else None,
