@@ -190,6 +190,8 @@ UT_API const char* ut_plan_probe(uint64_t base, uint64_t rows, uint64_t row_byte
  * the table violates returns UT_EINVAL and leaves the plan unchanged; every admissible kind is
  * correct for any output alignment (ut_gather falls back to "auto" for an output it cannot take).
  * "timing=on|off" brackets each gather-kernel launch with CUDA events (see ut_get_stats).
+ * "runs=on|off" (default off): for 16-B aligned tables, sort the rows exactly and copy runs of
+ * table-adjacent rows with one warp so shared boundary lines are requested once.
  * "conc=auto|dense|sparse" picks the launch shape: dense = every SM full of warps; sparse = a
  * quarter of the SMs, one row-step per warp (fewer translation pages in flight); auto = sparse
  * for reordered gathers from tables > 1 GiB.

@@ -12,6 +12,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libut.so")
 SOURCES = [os.path.join(CSRC, "ut.cu"), os.path.join(CSRC, "ut_sample.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "ut_kernels.cuh"), os.path.join(CSRC, "ut_internal.h"),
+                  os.path.join(CSRC, "ut_scan.cuh"),
                   os.path.join(INCLUDE, "ut.h")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

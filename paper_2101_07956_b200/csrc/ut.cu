@@ -22,6 +22,7 @@
 #include "ut.h"
 #include "ut_internal.h"
 #include "ut_kernels.cuh"
+#include "ut_scan.cuh"
 
 namespace utx {
 
@@ -276,6 +277,7 @@ struct ut_table {
   int reorder = -1;                     // -1 auto, 0 off, 1 on (ut_set_plan "reorder=...")
   bool timing = false;                  // ut_set_plan "timing=on"
   int conc = -1;                        // launch shape: -1 auto, 0 dense, 1 sparse ("conc=...")
+  int runs = -1;                        // run merge: -1 auto, 0 off, 1 on ("runs=...")
   std::mutex mu;
   DevState dev[kMaxDev];
 };
@@ -513,6 +515,9 @@ int bucket_shift(uint64_t table_bytes, uint64_t rb) {
   return shift;
 }
 
+bool want_runs(const ut_table* t, const Plan& p, uint64_t n);
+int gather_runs(const ut_table* t, DevState* s, const Plan& p, const ut::GatherArgs& a, cudaStream_t st);
+
 int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n, void* out_dev,
               cudaStream_t st, bool host_out = false, const uint64_t* n_dev = nullptr) {
   Plan p;
@@ -523,11 +528,13 @@ int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n
   cudaError_t e;
   s->rows += n;
   s->bytes += n * t->rb;
-  if (!want_reorder(t, n) || p.kind == P_PAPER_NAIVE || p.kind == P_PAPER_SHIFT) {
+  const bool runs = want_runs(t, p, n);
+  if (!runs && (!want_reorder(t, n) || p.kind == P_PAPER_NAIVE || p.kind == P_PAPER_SHIFT)) {
     e = timed_launch<false>(t, s, p, st, a, host_out);
     if (e != cudaSuccess) return cuda_err(e, plan_name(p));
     return UT_OK;
   }
+  if (runs) return gather_runs(t, s, p, a, st);
   // counting sort of the work items by 2-MiB table region (stream-ordered scratch from the
   // library's pool); n < 2^32 per launch, larger gathers are split.
   const int shift = bucket_shift(t->bytes, t->rb);
@@ -571,9 +578,9 @@ int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n
   return UT_OK;
 }
 
-template <bool PERM>
-cudaError_t timed_launch(const ut_table* t, DevState* s, const Plan& p, cudaStream_t st,
-                         const ut::GatherArgs& a, bool host_out) {
+// Bracket the gather kernel launched by `fn` with timing events when "timing=on".
+template <typename F>
+cudaError_t timed(const ut_table* t, DevState* s, cudaStream_t st, F&& fn) {
   std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
   if (t->timing) {
     std::lock_guard<std::mutex> lk(s->tmu);
@@ -586,7 +593,7 @@ cudaError_t timed_launch(const ut_table* t, DevState* s, const Plan& p, cudaStre
     }
     cudaEventRecord(ev.first, st);
   }
-  cudaError_t e = launch_plan<PERM>(p, s->sms, st, a, shape_for(t, s, PERM, a.n, host_out));
+  cudaError_t e = fn();
   if (e == cudaSuccess) {
     s->gathers += 1;
     s->launches += 1;
@@ -597,6 +604,12 @@ cudaError_t timed_launch(const ut_table* t, DevState* s, const Plan& p, cudaStre
     s->pending.push_back(ev);
   }
   return e;
+}
+
+template <bool PERM>
+cudaError_t timed_launch(const ut_table* t, DevState* s, const Plan& p, cudaStream_t st,
+                         const ut::GatherArgs& a, bool host_out) {
+  return timed(t, s, st, [&] { return launch_plan<PERM>(p, s->sms, st, a, shape_for(t, s, PERM, a.n, host_out)); });
 }
 
 Shape shape_for(const ut_table* t, const DevState* s, bool reordered, uint64_t n, bool host_out) {
@@ -614,6 +627,76 @@ Shape shape_for(const ut_table* t, const DevState* s, bool reordered, uint64_t n
                  t->alloc_kind != UT_ALLOC_MANAGED);
   int cap = env_blocks > 0 ? env_blocks : std::max(1, s->sms * 3 / 8);   // 55 of 148 SMs
   return Shape{sparse, cap};
+}
+
+// Run merge: sort the work items exactly by row id and copy each run of
+// table-adjacent rows with one warp, so their shared boundary lines are requested once. On the
+// products shape (19 % of rows have a selected neighbour, 4 % fewer line requests) the gather
+// kernel gains 1.9 % but the sort costs ~0.19 ms per 463K rows, a net loss of 2.6 % — so it is
+// opt-in ("runs=on"), never chosen by "auto" (profiles/r1_run_merge.log).
+bool want_runs(const ut_table* t, const Plan& p, uint64_t n) {
+  if (t->runs != 1 || (p.kind != P_VEC16 && p.kind != P_VEC16X)) return false;
+  return n < (1ull << 31);
+}
+
+int gather_runs(const ut_table* t, DevState* s, const Plan& p, const ut::GatherArgs& a0, cudaStream_t st) {
+  const uint64_t n = a0.n;
+  int shift = 12;                                   // buckets of ~64 rows, >= 4 KiB
+  while ((1ull << (shift + 1)) <= 64 * t->rb) ++shift;
+  while (((t->bytes - 1) >> shift) + 1 > (uint64_t)ut::kMaxBuckets) ++shift;
+  const uint32_t nb = (uint32_t)(((t->bytes - 1) >> shift) + 1);
+  const uint64_t tiles = n / kScanTile + 2;
+  // scratch (uint32 words): cnt[nb], perm[n], flags[n], pos[n], starts[n+1], sums[tiles],
+  // then two 8-byte words: the effective n and the run count
+  const size_t words = (size_t)nb + 4 * n + 1 + tiles + 6;
+  uint32_t* scratch = nullptr;
+  cudaError_t e;
+  if ((e = cudaMallocFromPoolAsync((void**)&scratch, words * sizeof(uint32_t), s->pool, st)) != cudaSuccess)
+    return cuda_err(e, "cudaMallocFromPoolAsync(run scratch)");
+  uint32_t* cnt = scratch;
+  uint32_t* perm = cnt + nb;
+  uint32_t* flags = perm + n;
+  uint32_t* pos = flags + n;
+  uint32_t* starts = pos + n;
+  uint32_t* sums = starts + n + 1;
+  uint64_t* words64 = (uint64_t*)(((uintptr_t)(sums + tiles) + 7) & ~(uintptr_t)7);
+  uint64_t* n_eff = words64;
+  uint64_t* n_runs = words64 + 1;
+  ut::GatherArgs a = a0;
+  a.perm = perm;
+  const uint64_t blocks = std::min<uint64_t>((uint64_t)s->sms * 2, (n + 2047) / 2048);
+  const uint64_t per_block = (n + blocks - 1) / blocks;
+  const int hsm = (int)(nb * sizeof(uint32_t));
+  static const bool smem_ok = [] {
+    const int mx = ut::kMaxBuckets * (int)sizeof(uint32_t);
+    return cudaFuncSetAttribute(ut::k_bucket_count, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess &&
+           cudaFuncSetAttribute(ut::k_bucket_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess &&
+           cudaFuncSetAttribute(ut::k_bucket_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess;
+  }();
+  if (!smem_ok) return set_err(UT_ECUDA, "cannot opt in to %d B of shared memory", hsm);
+  const int gb = (int)((n + 255) / 256);
+  ut::k_eff_n<<<1, 1, 0, st>>>(a0.n_dev, n, n_eff);
+  cudaMemsetAsync(cnt, 0, nb * sizeof(uint32_t), st);
+  ut::k_bucket_count<<<(int)blocks, 512, hsm, st>>>(a, shift, nb, per_block, cnt);
+  ut::k_bucket_scan<<<1, 1024, hsm, st>>>(cnt, nb);
+  ut::k_bucket_scatter<<<(int)blocks, 512, hsm, st>>>(a, shift, nb, per_block, cnt, perm);
+  ut::k_bucket_sort<<<(int)((nb + 255) / 256), 256, 0, st>>>(a, cnt, nb, perm);
+  ut::k_run_flags<<<gb, 256, 0, st>>>(a, flags);
+  scan_u32(flags, pos, n_eff, n, n_runs, sums, st);
+  ut::k_run_emit<<<gb, 256, 0, st>>>(a, flags, pos, n_runs, starts);
+  s->launches += 7 + (n > (uint64_t)kScanTile ? 3 : 2);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    e = timed(t, s, st, [&] {
+      auto k = ut::k_runs<kUx>;
+      ut::k_runs<kUx><<<grid_for(k, s->sms, n, -2), 256, 0, st>>>(a, starts, n_runs);
+      return cudaGetLastError();
+    });
+  }
+  cudaError_t e2 = cudaFreeAsync(scratch, st);
+  if (e != cudaSuccess) return cuda_err(e, "run-merge gather");
+  if (e2 != cudaSuccess) return cuda_err(e2, "cudaFreeAsync(run scratch)");
+  return UT_OK;
 }
 
 bool want_reorder(const ut_table* t, uint64_t n) {
@@ -1071,6 +1154,14 @@ int ut_set_plan(ut_table* t, const char* name) {
   if (!t || !name) return set_err(UT_EINVAL, "NULL argument");
   if (!strcmp(name, "timing=on") || !strcmp(name, "timing=off")) {
     t->timing = name[8] == 'n';
+    return UT_OK;
+  }
+  if (!strncmp(name, "runs=", 5)) {
+    const char* v = name + 5;
+    if (!strcmp(v, "auto")) t->runs = -1;
+    else if (!strcmp(v, "on")) t->runs = 1;
+    else if (!strcmp(v, "off")) t->runs = 0;
+    else return set_err(UT_EINVAL, "runs must be auto|on|off, got '%s'", v);
     return UT_OK;
   }
   if (!strncmp(name, "conc=", 5)) {

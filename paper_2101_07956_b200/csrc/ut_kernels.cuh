@@ -559,4 +559,104 @@ __global__ void __launch_bounds__(512) k_bucket_scatter(GatherArgs a_, int shift
     perm[atomicAdd(&hist[bucket_of(a, i, shift)], 1u)] = (uint32_t)i;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Run merge: with the work items in exact table order, rows that are neighbours in
+// the table form runs; one warp copies a run's contiguous byte span through 128-B-aligned windows,
+// so the line two adjacent rows share is requested once instead of twice (two partial requests).
+// Only for 16-B aligned tables and outputs with rb % 16 == 0: a 16-B chunk then lies in one row.
+
+// Exact order inside each (small) bucket: one thread insertion-sorts its bucket's work items by
+// row id. ends[] = bucket ends after k_bucket_scatter. Buckets above 256 items are left as they
+// are (order only affects how many runs are found, never the result).
+__global__ void __launch_bounds__(256) k_bucket_sort(GatherArgs a_, const uint32_t* __restrict__ ends,
+                                                     uint32_t nb, uint32_t* perm) {
+  const GatherArgs a = with_dev_n(a_);
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const uint32_t lo = b ? ends[b - 1] : 0u, hi = ends[b];
+  if (hi - lo < 2 || hi - lo > 256) return;
+  for (uint32_t x = lo + 1; x < hi; ++x) {
+    const uint32_t item = perm[x];
+    const uint64_t key = (uint64_t)__ldg(a.idx + item);
+    uint32_t y = x;
+    while (y > lo && (uint64_t)__ldg(a.idx + perm[y - 1]) > key) {
+      perm[y] = perm[y - 1];
+      --y;
+    }
+    perm[y] = item;
+  }
+}
+
+// flags[j] = 1 where work item j starts a run (its row is not the successor of item j-1's row).
+__global__ void __launch_bounds__(256) k_run_flags(GatherArgs a_, uint32_t* __restrict__ flags) {
+  const GatherArgs a = with_dev_n(a_);
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.n) return;
+  const uint64_t r = (uint64_t)__ldg(a.idx + a.perm[j]);
+  uint32_t start = 1u;
+  if (j > 0 && r < a.rows) {
+    const uint64_t rp = (uint64_t)__ldg(a.idx + a.perm[j - 1]);
+    start = (rp < a.rows && r == rp + 1) ? 0u : 1u;
+  }
+  flags[j] = start;
+}
+
+// *out = the effective row count: min(*n_dev, n) when the count lives on the device, else n.
+__global__ void k_eff_n(const uint64_t* n_dev, uint64_t n, uint64_t* out) {
+  *out = (n_dev && *n_dev < n) ? *n_dev : n;
+}
+
+// run_start[pos[j]] = j for run starts; run_start[n_runs] = n.
+__global__ void __launch_bounds__(256) k_run_emit(GatherArgs a_, const uint32_t* __restrict__ flags,
+                                                  const uint32_t* __restrict__ pos,
+                                                  const uint64_t* n_runs, uint32_t* run_start) {
+  const GatherArgs a = with_dev_n(a_);
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.n) return;
+  if (flags[j]) run_start[pos[j]] = (uint32_t)j;
+  if (j == 0) run_start[*n_runs] = (uint32_t)a.n;
+}
+
+template <int U>
+__global__ void __launch_bounds__(256) k_runs(GatherArgs a_, const uint32_t* __restrict__ run_start,
+                                              const uint64_t* n_runs) {
+  const GatherArgs a = with_dev_n(a_);
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t nr = *n_runs;
+  for (uint64_t run = warp; run < nr; run += nwarps) {
+    const uint32_t j0 = run_start[run], j1 = run_start[run + 1];
+    const uint64_t i0 = a.perm[j0];
+    const uint64_t r0 = (uint64_t)__ldg(a.idx + i0);
+    if (r0 >= a.rows) {        // an out-of-range index is a run of one: zero row + record
+      const uint64_t d = a.out + i0 * a.rb;
+      for (uint64_t c = (uint64_t)lane * 16; c < a.rb; c += 32 * 16) st16(d + c, v4_zero());
+      if (lane == 0) record_bad(a.err, i0);
+      continue;
+    }
+    const uint64_t s = a.tbase + r0 * a.rb;
+    const uint64_t send = s + (uint64_t)(j1 - j0) * a.rb;
+    const uint64_t ws = s & ~127ull;
+    const uint64_t nch = (((send + 15) & ~15ull) - ws) >> 4;
+    for (uint64_t c0 = 0; c0 < nch; c0 += 32 * U) {
+      V4 cur[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t A = ws + 16ull * (c0 + 32u * u + lane);
+        cur[u] = (A >= s && A < send) ? ld_table16(A) : v4_zero();
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t A = ws + 16ull * (c0 + 32u * u + lane);
+        if (A >= s && A < send) {
+          const uint64_t rel = A - s;
+          const uint64_t k = rel / a.rb;
+          st16(a.out + (uint64_t)a.perm[j0 + k] * a.rb + (rel - k * a.rb), cur[u]);
+        }
+      }
+    }
+  }
+}
+
 }  // namespace ut

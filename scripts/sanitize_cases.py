@@ -26,7 +26,7 @@ for rb, off in [(4, 0), (8, 8), (68, 3), (400, 0), (400, 4), (2052, 1), (4096, 0
                 t.set_plan(plan)
             except ut.UTError:
                 continue
-            for reorder in ["reorder=off", "reorder=on"]:
+            for reorder in ["reorder=off", "reorder=on", "runs=on"]:
                 t.set_plan(reorder)
                 buf = torch.zeros(700 * rb + 16, dtype=torch.uint8, device="cuda")
                 t.gather(torch.from_numpy(idx).cuda(), out=buf[off: off + 700 * rb])

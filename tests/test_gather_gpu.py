@@ -92,6 +92,7 @@ def test_randomized_instances(pinned_pool):
             if rng.random() < 0.4:
                 t.set_plan("reorder=on")                # translation-locality visiting order
             t.set_plan("conc=" + rng.choice(["auto", "dense", "sparse"]))   # launch shape
+            t.set_plan("runs=" + rng.choice(["auto", "on", "off"]))          # run merge
             plan = rng.choice(plans)
             if plan is not None:
                 try:
@@ -255,3 +256,24 @@ def test_create_library_owned_table(kind, rb):
         workloads.fill_table(t.host_addr, rows, rb, 31)
         out = t[torch.from_numpy(idx).cuda()]
         assert out.cpu().numpy().tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("rb,off", [(16, 0), (400, 0), (512, 0), (2048, 0), (400, 16)])
+def test_run_merge_dense_and_adjacent(rb, off):
+    """Run merge (vec16 tables): identity, contiguous ranges, shuffled dense selections,
+    duplicates and out-of-range indices, with run merge forced on and off."""
+    rows = 6000
+    hb = workloads.HostBuffer(rows * rb, offset=off)
+    workloads.fill_table(hb.addr, rows, rb, 77)
+    rng = np.random.default_rng(rb)
+    cases = [np.arange(rows), np.arange(100, 900), rng.permutation(rows)[:3000],
+             np.sort(rng.choice(rows, 2500, replace=False)), rng.integers(0, rows, 4000)]
+    bad = rng.permutation(rows)[:2000].astype(np.int64)
+    bad[[3, 700, 1999]] = [rows, -1, rows + 5]
+    cases.append(bad)
+    with ut.Table(hb.addr, rows, rb) as t:
+        for mode in ["runs=on", "runs=off"]:
+            t.set_plan(mode)
+            for c in cases:
+                _gather_check(t, hb.addr, rows, rb, np.asarray(c, dtype=np.int64))
+    hb.close()
