@@ -361,6 +361,12 @@ def run_ut(args, spec, dist):
 
     tag = f"{spec['config'].replace(':', '_')}_{os.environ.get('MASTER_PORT', '0')}"
     t_reg = time.perf_counter()
+    if args.alloc == "auto":
+        # the paper's own allocation (managed memory + its cudaMemAdvise) is the fastest table
+        # memory beyond the ~1-GiB translation reach but is process-private; one
+        # shared registered table is the only way for N ranks to hold a single copy
+        big = spec["rows"] * spec["row_bytes"] > (1 << 30)
+        args.alloc = "managed" if (world == 1 and big) else "register"
     if args.alloc == "register":
         hb = open_table(spec, rank, world, seed, dist, tag)
         t_reg = time.perf_counter()
@@ -807,8 +813,9 @@ def main(argv=None):
     ap.add_argument("--no-check", dest="check", action="store_false")
     ap.add_argument("--backend", default="nccl", help="process-group backend at N > 1")
     ap.add_argument("--presort", action="store_true", help="experiment: sort index lists on the host")
-    ap.add_argument("--alloc", default="register", choices=["register", "pinned", "managed", "vmm"],
-                    help="table memory: caller mmap + ut_register (default) or ut_create(kind)")
+    ap.add_argument("--alloc", default="auto", choices=["auto", "register", "pinned", "managed", "vmm"],
+                    help="table memory: caller mmap + ut_register, or ut_create(kind); auto = "
+                         "managed for one rank and a table > 1 GiB, else register")
     ap.add_argument("--sample", default="cpu", choices=["cpu", "gpu"],
                     help="cpu: index lists sampled before timing (default, the paper's split); "
                          "gpu: ut_sample inside every timed step (SURVEY NEXT-2)")

@@ -277,3 +277,39 @@ def test_run_merge_dense_and_adjacent(rb, off):
             for c in cases:
                 _gather_check(t, hb.addr, rows, rb, np.asarray(c, dtype=np.int64))
     hb.close()
+
+
+def test_concurrent_gathers_from_threads_and_streams():
+    """The header's threading claim: concurrent ut_gather calls on one table from several host
+    threads, each on its own stream, are safe and each result is exact."""
+    import threading
+    rows, rb = 50_000, 400
+    hb = workloads.HostBuffer(rows * rb)
+    workloads.fill_table(hb.addr, rows, rb, 91)
+    lists = [workloads.uniform_idx(20_000 + 997 * k, rows, 100 + k) for k in range(6)]
+    wants = [oracle.gather(hb.addr, rows, rb, l)[0] for l in lists]
+    errors = []
+    with ut.Table(hb.addr, rows, rb) as t:
+        def work(k):
+            try:
+                s = torch.cuda.Stream()
+                with torch.cuda.stream(s):
+                    idx = torch.from_numpy(lists[k]).cuda()
+                    for rep in range(5):
+                        if k % 2:
+                            t.set_plan("timing=on")
+                        out = t.gather(idx, stream=s)
+                        s.synchronize()
+                        if out.cpu().numpy().tobytes() != wants[k].tobytes():
+                            errors.append((k, rep))
+            except Exception as e:   # pragma: no cover - reported below
+                errors.append((k, repr(e)))
+        th = [threading.Thread(target=work, args=(k,)) for k in range(6)]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+        assert not errors, errors
+        st = t.stats()
+        assert st["gathers"] >= 30 and st["timed_launches"] <= st["gathers"]
+    hb.close()
