@@ -1,0 +1,34 @@
+"""The C ABI from plain C (examples/c_gather.c): compiles here against include/ut.h and
+libut.so; runs on a B200 (-m gpu) and checks bytes against a memcpy loop."""
+import os
+import subprocess
+
+import pytest
+
+import paper_2101_07956_b200 as ut
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+EXE = os.path.join(ROOT, "build", "c_gather")
+
+
+def _compile():
+    os.makedirs(os.path.dirname(EXE), exist_ok=True)
+    libdir = os.path.dirname(ut.LIB_PATH)
+    cmd = ["gcc", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           os.path.join(ROOT, "examples", "c_gather.c"), "-L", libdir, "-lut",
+           "-L", "/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{libdir}",
+           "-Wl,-rpath,/usr/local/cuda/lib64", "-o", EXE]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+
+
+def test_c_example_compiles():
+    _compile()
+    assert os.path.exists(EXE)
+
+
+@pytest.mark.gpu
+def test_c_example_runs():
+    _compile()
+    p = subprocess.run([EXE], capture_output=True, text=True, timeout=120)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "C-ABI OK" in p.stdout
