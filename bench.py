@@ -70,7 +70,7 @@ def make_index_lists(spec: dict, rank: int, world: int, count: int, seed: int,
                 for b in range(count)]
     jobs = [(spec["config"], seed, b, rank, world, False) for b in range(count)]
     if procs > 1 and count > 1:
-        with mp.get_context("fork").Pool(min(procs, count)) as pool:
+        with mp.get_context("spawn").Pool(min(procs, count)) as pool:
             return pool.map(graphsage.minibatch_job, jobs)
     return [graphsage.minibatch_job(j) for j in jobs]
 

@@ -38,7 +38,7 @@ def _check_lists(spec, lists, extra_plans=()):
 @pytest.mark.parametrize("config", ["tiny", "reddit", "products", "papers"])
 def test_paper_shaped_configs_full_minibatches(config):
     spec = bench.workload_spec(config)
-    lists = bench.make_index_lists(spec, 0, 1, 2, 2101 + 17, 4)
+    lists = bench.make_index_lists(spec, 0, 1, 2, 2101 + 17, 1)
     # rank 1 of 2 as well: the sharded path is the same gather on another root slice
     lists += bench.make_index_lists(spec, 1, 2, 1, 2101 + 17, 1)
     _check_lists(spec, lists, extra_plans=("conc=dense", "conc=auto") if config == "papers" else ())
