@@ -83,11 +83,13 @@ def open_table(spec: dict, rank: int, world: int, seed: int, dist, tag: str):
     threads = os.cpu_count() or 1
     if world == 1:
         hb = workloads.HostBuffer(nbytes)
+        hb.numa = workloads.interleave(hb.addr, nbytes)
         workloads.fill_table(hb.addr, rows, rb, seed, threads=threads)
         return hb
     name = f"ut_bench_{tag}"
     if rank == 0:
         hb = workloads.HostBuffer(nbytes, kind="shm", name=name, create=True)
+        hb.numa = workloads.interleave(hb.addr, nbytes)    # one copy for every socket's GPUs
         workloads.fill_table(hb.addr, rows, rb, seed, threads=threads)
     dist.barrier()
     if rank != 0:
@@ -356,6 +358,10 @@ def run_ut(args, spec, dist):
 
     ndev = torch.cuda.device_count()
     torch.cuda.set_device(dist.local_rank % ndev)     # > 1 rank per GPU only with --backend gloo
+    # host threads of this rank next to its GPU; no-op on single-node boxes
+    gnode = workloads.gpu_numa_node(torch.cuda.current_device())
+    if gnode >= 0 and workloads.numa_nodes() > 1 and workloads.node_cpus(gnode):
+        os.sched_setaffinity(0, workloads.node_cpus(gnode))
     dist.init(args.backend)
     import paper_2101_07956_b200 as ut
 
@@ -547,14 +553,18 @@ def run_ut(args, spec, dist):
 
     if rank == 0:
         n_launch = int(launches)
+        cfg = config_block(spec, lists[args.warmup:] or lists, world)
+        sect_ratio = (cfg["sector_floor_mb_per_step"] / cfg["mb_per_step_per_gpu"]
+                      if cfg.get("mb_per_step_per_gpu") else None)
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(max_dev_ms / args.steps, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (self-identifying fp32-row table, GraphSAGE-shaped index lists)",
-            "config": config_block(spec, lists[args.warmup:] or lists, world),
+            "config": cfg,
             "per_gpu_gbs": round(per_gpu, 3),
+            "transferred_gbs_sector_floor": round(value * sect_ratio, 3) if sect_ratio else None,
             "h2d_memcpy_gbs": round(link, 3),
             "h2d_memcpy_concurrent_gbs": round(link_sum, 3),
             "host_dram_read_gbs": dram,
@@ -563,6 +573,8 @@ def run_ut(args, spec, dist):
             "sm_read_ceiling_gbs": round(sm_ceiling, 3),
             "frac_of_sm_read_ceiling": round(per_gpu / sm_ceiling, 4),
             "plan": table.plan, "table_memory": args.alloc,
+            "numa": {"nodes": workloads.numa_nodes(), "gpu_node": gnode,
+                     "table_policy": "interleave" if getattr(hb, "numa", 0) > 1 else "single node / default"},
             "roofline": {"bound": "pcie_h2d",
                          "achieved": round(achieved, 3) if achieved is not None else None,
                          "peak": round(link, 3), "unit": "GB/s",

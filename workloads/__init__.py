@@ -54,6 +54,10 @@ def lib():
         L.gen_chunglu_indices.restype = None
         L.gen_chunglu_indices.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
                                           ctypes.c_double, ctypes.c_uint64, ctypes.c_int]
+        L.gen_numa_nodes.restype = ctypes.c_int
+        L.gen_numa_nodes.argtypes = []
+        L.gen_interleave.restype = ctypes.c_int
+        L.gen_interleave.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
         L.gen_map.restype = ctypes.c_void_p
         L.gen_map.argtypes = [ctypes.c_uint64, ctypes.c_int]
         L.gen_unmap.restype = ctypes.c_int
@@ -90,6 +94,38 @@ def uniform_idx(n: int, rows: int, seed: int) -> np.ndarray:
     if n:
         lib().gen_uniform_idx(out.ctypes.data, n, rows, seed & 0xFFFFFFFFFFFFFFFF)
     return out
+
+
+def numa_nodes() -> int:
+    return int(lib().gen_numa_nodes())
+
+
+def interleave(addr: int, nbytes: int) -> int:
+    """Interleave the pages of [addr, addr+nbytes) over all NUMA nodes before first touch.
+    Returns the node count used (0: single node, nothing to do; -1: mbind failed)."""
+    return int(lib().gen_interleave(addr, nbytes))
+
+
+def gpu_numa_node(device_index: int = 0) -> int:
+    """NUMA node of a CUDA device from sysfs (-1 when unknown)."""
+    try:
+        import torch
+        p = torch.cuda.get_device_properties(device_index)
+        path = f"/sys/bus/pci/devices/{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0/numa_node"
+        return int(open(path).read().strip())
+    except Exception:
+        return -1
+
+
+def node_cpus(node: int) -> list[int]:
+    cpus = []
+    try:
+        for part in open(f"/sys/devices/system/node/node{node}/cpulist").read().strip().split(","):
+            a, _, b = part.partition("-")
+            cpus.extend(range(int(a), int(b or a) + 1))
+    except OSError:
+        pass
+    return cpus
 
 
 def decode_row_ids(rows_bytes: np.ndarray, rb: int) -> np.ndarray:

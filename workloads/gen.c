@@ -153,3 +153,31 @@ void gen_chunglu_indices(const int64_t* indptr, int32_t* indices, uint64_t N, do
         }
     }
 }
+
+/* ---- NUMA placement of a table (NUMA-interleaved by default) ------------------
+ * mbind(MPOL_INTERLEAVE) over all online nodes before first touch. Returns the number of nodes
+ * used (0 when the kernel has no NUMA support or a single node: nothing to do). */
+#include <sys/syscall.h>
+#include <stdio.h>
+
+int gen_numa_nodes(void)
+{
+    int n = 0;
+    for (int i = 0; i < 1024; ++i) {
+        char path[96];
+        snprintf(path, sizeof path, "/sys/devices/system/node/node%d", i);
+        if (access(path, F_OK) == 0) ++n;
+        else if (i > 64 && n) break;
+    }
+    return n;
+}
+
+int gen_interleave(void* addr, uint64_t bytes)
+{
+    int nodes = gen_numa_nodes();
+    if (nodes <= 1) return 0;
+    unsigned long mask[16] = {0};
+    for (int i = 0; i < nodes && i < 1024; ++i) mask[i / 64] |= 1ul << (i % 64);
+    long rc = syscall(SYS_mbind, addr, bytes, 3 /* MPOL_INTERLEAVE */, mask, 1024ul, 0u);
+    return rc == 0 ? nodes : -1;
+}
