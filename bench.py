@@ -68,7 +68,8 @@ def make_index_lists(spec: dict, rank: int, world: int, count: int, seed: int,
     if spec["kind"] == "uniform":
         return [workloads.uniform_idx(spec["n"], spec["rows"], seed=seed + 1000003 * (b * world + rank))
                 for b in range(count)]
-    jobs = [(spec["config"], seed, b, rank, world, False) for b in range(count)]
+    rev = bool(spec.get("reverse_fanouts"))
+    jobs = [(spec["config"], seed, b, rank, world, rev) for b in range(count)]
     if procs > 1 and count > 1:
         with mp.get_context("spawn").Pool(min(procs, count)) as pool:
             return pool.map(graphsage.minibatch_job, jobs)
@@ -839,12 +840,17 @@ def main(argv=None):
                     help="with --sample gpu: capture sample + gather once in a CUDA graph, replay")
     ap.add_argument("--pipeline", action="store_true",
                     help="with --sample gpu: sample minibatch k+1 while gathering minibatch k")
+    ap.add_argument("--reverse-fanouts", action="store_true",
+                    help="graphsage configs: apply the fanouts in reverse hop order (SURVEY c15)")
     ap.add_argument("--allreduce-smoke", action="store_true",
                     help="N > 1: one untimed NCCL all-reduce of a 4-MB fp32 buffer after timing")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
     spec = workload_spec(args.config)
+    if args.reverse_fanouts and spec["kind"] == "graphsage":
+        spec["reverse_fanouts"] = True          # DGL's order: the last fanout at the seeds (c15)
+        spec["fanouts"] = list(reversed(spec["fanouts"]))
     dist = Dist()
     try:
         if args.impl == "reference":
