@@ -21,6 +21,7 @@ cores on the same workload, as the reference arm.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import multiprocessing as mp
 import os
@@ -249,6 +250,30 @@ def sm_read_ceiling(torch, ut, nbytes: int = 1 << 30, reps: int = 5) -> float:
     return best
 
 
+NCU_TRAFFIC = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+
+
+def ncu_traffic(workload: str, plan: str, args) -> dict:
+    """roofline.traffic from the committed ncu capture of this workload's timed gathers
+    (profiles/ncu_traffic.json, written by scripts/ncu_summary.py --traffic): HBM bytes
+    (dram__bytes_read.sum + dram__bytes_write.sum) per gather launch, averaged over the captured
+    launches, next to the link-side bytes (sysmem sectors x 32) and the algorithmic bytes (n*rb)
+    of the same launches. null when no capture matches the workload and plan."""
+    try:
+        with open(NCU_TRAFFIC) as f:
+            rec = json.load(f).get(workload)
+    except (OSError, ValueError):
+        rec = None
+    if not rec or rec.get("plan") != plan or args.plan or args.sample != "cpu":
+        return {"traffic": None}
+    return {"traffic": rec["hbm_bytes_per_launch"],
+            "traffic_detail": {k: rec[k] for k in ("hbm_bytes_per_launch", "hbm_write_bytes_per_launch",
+                                                   "sysmem_bytes_per_launch", "sysmem_requests_per_launch",
+                                                   "pcie_read_bytes_per_launch",
+                                                   "algorithmic_bytes_per_launch", "launches",
+                                                   "source") if k in rec}}
+
+
 def cpu_oracle_rate(table_addr: int, spec: dict, lists: list[np.ndarray], budget_s: float):
     """The oracle as it stands, on this host, over a bounded sample of the same index lists."""
     import oracle
@@ -443,6 +468,8 @@ def run_ut(args, spec, dist):
     nbytes = 0
     dist.barrier()
     torch.cuda.synchronize()
+    # NVTX range "timed": ncu's --nvtx --nvtx-include "timed/" profiles exactly these launches
+    torch.cuda.nvtx.range_push("timed")
     t0 = time.perf_counter()
     if sampler is not None and args.pipeline:
         # sample minibatch k+1 (its own stream) while minibatch k is gathered: the whole loop is
@@ -464,6 +491,7 @@ def run_ut(args, spec, dist):
         e1.record(stream)
         evs.append((e0, e1))
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     if sampler is not None and sampler.mode != "sync":
         nbytes += sampler.device_rows() * rb
     dist.barrier()
@@ -580,7 +608,7 @@ def run_ut(args, spec, dist):
                          "achieved": round(achieved, 3) if achieved is not None else None,
                          "peak": round(link, 3), "unit": "GB/s",
                          "frac": round(achieved / link, 4) if achieved is not None else None,
-                         "traffic": None,
+                         **ncu_traffic(spec["workload"], table.plan, args),
                          "kernel": f"gather {table.plan} (device time of the gather kernel alone, CUDA events on its stream)",
                          "peak_source": "pinned cudaMemcpy H2D measured in this run (best of 10 x 1 GiB)",
                          "sm_read_ceiling": round(sm_ceiling, 3)},
@@ -785,7 +813,11 @@ class GpuSampling:
 
 
 def cpu_staged_baseline(torch, table_addr, spec, lists, args):
-    """The paper's "Py" path (Fig. 2a): all host cores gather into pinned staging, one H2D DMA."""
+    """The paper's "Py" path (Fig. 2a): all host cores gather into pinned
+    staging, then one H2D DMA. Three forms: sequential (paper-faithful), double-
+    buffered (chunk k+1 gathered while chunk k is in flight: the stronger CPU-centric baseline),
+    and pageable (Listing 1 literally, `features[neighbor_id].to("cuda")`, PAPER.md:315-316,
+    torch's own CPU index_select into pageable memory)."""
     import baselines
     rb = spec["row_bytes"]
     max_n = max(l.size for l in lists)
@@ -793,21 +825,61 @@ def cpu_staged_baseline(torch, table_addr, spec, lists, args):
     dev = torch.empty(max_n * rb, dtype=torch.uint8, device="cuda")
     threads = os.cpu_count() or 1
     steps = min(len(lists), max(3, args.steps // 2))
-    sec, nbytes = 0.0, 0
-    for s in range(steps + 1):
-        l = lists[s % len(lists)]
+    chunks = 8
+    copy_stream = torch.cuda.Stream()
+
+    def sequential(l):
         b = l.size * rb
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
         baselines.cpu_staged_gather(table_addr, rb, l.ctypes.data, l.size, staging.data_ptr(), threads)
         dev[:b].copy_(staging[:b], non_blocking=True)
-        torch.cuda.synchronize()
-        if s > 0:
-            sec += time.perf_counter() - t0
-            nbytes += b
-    return {"value": round(nbytes / sec / 1e9, 3), "unit": "GB/s", "threads": threads,
-            "kind": "CPU gather into pinned staging + cudaMemcpyAsync H2D (PAPER.md:221-225)",
-            "steps": steps}
+
+    def double_buffered(l):
+        # two halves of the staging buffer alternate; chunk c is gathered into half c % 2 once
+        # the DMA of chunk c - 2 (same half) has drained
+        per = (l.size + chunks - 1) // chunks
+        half = ((per * rb + 4095) // 4096) * 4096
+        done = [None, None]
+        for c in range(chunks):
+            lo, hi = c * per, min(l.size, (c + 1) * per)
+            if lo >= hi:
+                break
+            h = c % 2
+            if done[h] is not None:
+                done[h].synchronize()
+            baselines.cpu_staged_gather(table_addr, rb, l.ctypes.data + 8 * lo, hi - lo,
+                                        staging.data_ptr() + h * half, threads)
+            with torch.cuda.stream(copy_stream):
+                dev[lo * rb:hi * rb].copy_(staging[h * half:h * half + (hi - lo) * rb], non_blocking=True)
+                done[h] = torch.cuda.Event()
+                done[h].record(copy_stream)
+        copy_stream.synchronize()
+
+    buf = (ctypes.c_uint8 * (spec["rows"] * rb)).from_address(table_addr)
+    table_view = torch.frombuffer(buf, dtype=torch.uint8).view(spec["rows"], rb)
+
+    def pageable(l):
+        table_view[torch.from_numpy(l)].to("cuda")
+
+    def rate(fn):
+        sec, nbytes = 0.0, 0
+        for s in range(steps + 1):
+            l = lists[s % len(lists)]
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn(l)
+            torch.cuda.synchronize()
+            if s > 0:
+                sec += time.perf_counter() - t0
+                nbytes += l.size * rb
+        return round(nbytes / sec / 1e9, 3)
+
+    out = {"value": rate(sequential), "unit": "GB/s", "threads": threads,
+           "kind": "CPU gather into pinned staging + cudaMemcpyAsync H2D (PAPER.md:221-225)",
+           "steps": steps, "double_buffered": rate(double_buffered),
+           "double_buffered_chunks": chunks}
+    out["pageable"] = rate(pageable)
+    out["pageable_kind"] = "torch CPU index_select + pageable .to('cuda') (Listing 1, PAPER.md:315-316)"
+    return out
 
 
 def main(argv=None):

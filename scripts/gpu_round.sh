@@ -15,14 +15,17 @@ for c in reddit papers tiny; do
   timeout 1200 python bench.py --config $c --steps 50 > $R/bench_$c.json 2> $R/bench_$c.err
 done
 timeout 1200 python bench.py --config papers --alloc register --steps 50 --no-cpu > $R/bench_papers_registered.json 2>> $R/bench_papers.err
-for rb in 4 8 16 32 64 68 100 128 256 400 512 1024 1372 2048 2052 2408 4096; do
+for rb in 4 8 16 32 64 68 100 128 132 256 260 400 512 516 1024 1028 1172 1372 2048 2052 2056 2064 2076 2408 3200 4092 4096; do
   timeout 600 python bench.py --config sweep:$rb --steps 10 --warmup 3 --no-cpu --no-e2e --max-lists 13 >> $R/bench_sweep.jsonl 2>> $R/bench_sweep.err
 done
 for c in products papers; do
   timeout 900 python bench.py --config $c --sample gpu --graph --graph-indptr "hbm,indices=hbm" --steps 30 --no-cpu --max-lists 16 >> $R/bench_gpu_sampling.jsonl 2>> $R/bench_gpu_sampling.err
 done
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $R/launches_products.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --max-lists 6 > /dev/null 2>&1
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $R/launches_papers.csv python bench.py --config papers --steps 3 --warmup 3 --no-e2e --no-cpu --max-lists 6 > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_single -s 4 -c 1 -o $R/prof_products python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --max-lists 6 > $R/ncu_full.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_single -s 4 -c 1 -o $R/prof_papers python bench.py --config papers --steps 3 --warmup 3 --no-e2e --no-cpu --max-lists 6 > $R/ncu_full_papers.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_multi -s 4 -c 1 -o $R/prof_reddit python bench.py --config reddit --steps 3 --warmup 3 --no-e2e --no-cpu --max-lists 6 > $R/ncu_full_reddit.log 2>&1
+# ncu: only launches inside bench.py's NVTX "timed" range (the probes before it are excluded)
+NV='--nvtx --nvtx-include timed/'
+TM=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,syslts__t_sectors_aperture_sysmem_op_read.sum,syslts__t_requests_aperture_sysmem_op_read.sum,pcie__read_bytes.sum
+for c in products papers reddit; do
+  timeout 900 ncu $NV --metrics gpu__time_duration.sum --clock-control none --csv --log-file $R/launches_$c.csv python bench.py --config $c --steps 6 --warmup 3 --no-e2e --no-cpu --max-lists 9 > /dev/null 2>&1
+  timeout 900 ncu $NV -k regex:'k_(single|multi|narrow|runs)' --metrics $TM --clock-control none --csv --log-file $R/traffic_$c.csv python bench.py --config $c --steps 6 --warmup 3 --no-e2e --no-cpu --max-lists 9 > $R/traffic_$c.json 2> $R/traffic_$c.err
+  timeout 900 ncu $NV -k regex:'k_single|k_multi' -s 2 -c 1 --set full --clock-control none --import-source on -o $R/prof_$c python bench.py --config $c --steps 6 --warmup 3 --no-e2e --no-cpu --max-lists 9 > $R/ncu_full_$c.log 2>&1
+done
