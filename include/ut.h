@@ -315,6 +315,97 @@ typedef struct ut_table_info {
 /* Fill *info. Returns UT_OK or UT_EINVAL. */
 UT_API int ut_table_get_info(const ut_table* t, ut_table_info* info);
 
+/* ============================================================================================
+ * Cooperative multi-rank gather.
+ *
+ * Several ranks (one process per GPU, or several processes sharing a GPU) gather their own
+ * minibatches from one host table in the same step. The paper has each GPU read its rows over
+ * its own link (Fig. 2b), so rows sampled by several ranks cross the host side
+ * once per rank. Here the table's rows are split into blocks owned round-robin by the ranks
+ * (ut_coop_owner); a step sends each index to its owner (P2P stores into the owner's inbox in
+ * device memory), each owner fetches the union of the rows it was asked for ONCE from host memory
+ * with ut_gather_dn, and each rank copies its rows from the owners' staging rows (P2P loads) into
+ * its output in index order. The result is exactly ut_gather's: out[i*rb..(i+1)*rb) = row idx[i]
+ * (PAPER.md:377); out-of-range indices give a zero row and a recorded position (reading R4).
+ *
+ * Setup: every rank calls ut_coop_create (same world, max_n and table shape on every rank; each
+ * rank registers the table itself), ut_coop_export, moves the handles to every rank (the caller's
+ * plumbing, e.g. torch.distributed all_gather_object), then ut_coop_open with all handles in rank
+ * order. A step is either
+ *   (a) ut_coop_gather on every rank: phases synchronised on the device (stream memory
+ *       operations on flag words in peer memory; no host round trip), or
+ *   (b) ut_coop_dispatch; [stream sync + host barrier of all ranks]; ut_coop_fetch;
+ *       [stream sync + host barrier]; ut_coop_combine — the caller synchronises.
+ * Every rank must take part in every step (n may be 0). Buffers are double-buffered by step
+ * parity, so consecutive steps need no extra barrier. Not thread-safe per handle.
+ * ============================================================================================ */
+typedef struct ut_coop ut_coop;
+
+#define UT_COOP_HANDLE_BYTES 64
+
+/* Create this rank's side on the CURRENT device. t: this process's handle of the shared table.
+ * world in [1, 64], rank in [0, world); max_n: the largest n any rank passes per step, with
+ * world*max_n < 2^31. Allocates the rank's symmetric device region (2 x (inboxes world*max_n*12 B
+ * + staging world*max_n*rb B)) and private scratch (a dedup tag table of ~rows/world x 8 B).
+ * world == 1 needs no ut_coop_open. NULL on failure (ut_last_error). */
+UT_API ut_coop* ut_coop_create(const ut_table* t, int world, int rank, uint64_t max_n);
+
+/* Write the CUDA IPC handle (UT_COOP_HANDLE_BYTES bytes) of this rank's region to handle_out and
+ * its size to *region_bytes (may be NULL). Returns UT_OK, UT_EINVAL or UT_ECUDA. */
+UT_API int ut_coop_export(const ut_coop* c, void* handle_out, uint64_t* region_bytes);
+
+/* Map every other rank's region: handles = world x UT_COOP_HANDLE_BYTES bytes in rank order
+ * (this rank's entry is ignored). Returns UT_OK, UT_EINVAL or UT_ECUDA. */
+UT_API int ut_coop_open(ut_coop* c, const void* handles);
+
+/* Phase 1: send idx_dev[0..n) (device memory, int64, caller-owned, n <= max_n) to the owners.
+ * Starts a new step. Asynchronous on `stream`. Returns UT_OK, UT_EINVAL or UT_ECUDA. */
+UT_API int ut_coop_dispatch(ut_coop* c, const int64_t* idx_dev, uint64_t n, ut_stream_t stream);
+
+/* Phase 2 (after every rank's phase 1 completed): deduplicate the requests this rank owns and
+ * gather the unique rows from host memory into its staging rows. Asynchronous on `stream`. */
+UT_API int ut_coop_fetch(ut_coop* c, ut_stream_t stream);
+
+/* Phase 3 (after every rank's phase 2 completed): out_dev[i*rb ..) = row idx[i] of this step's
+ * dispatch (>= n*rb bytes of device memory, any alignment). Asynchronous on `stream`. */
+UT_API int ut_coop_combine(ut_coop* c, void* out_dev, ut_stream_t stream);
+
+/* The three phases with device-side barriers between them (every rank calls it for the step).
+ * Returns UT_OK, UT_EINVAL, UT_ENOTSUP (no stream memory operations) or UT_ECUDA. */
+UT_API int ut_coop_gather(ut_coop* c, const int64_t* idx_dev, uint64_t n, void* out_dev,
+                          ut_stream_t stream);
+
+typedef struct ut_coop_stats {
+  uint64_t steps;                /* steps dispatched by this rank                                */
+  uint64_t requested_rows;       /* sum of this rank's n                                         */
+  uint64_t owner_requests;       /* requests this rank received as an owner (all sources)        */
+  uint64_t unique_rows_fetched;  /* rows this rank fetched from host memory as an owner          */
+  uint64_t last_unique_rows;     /* ... in the last fetch                                        */
+  uint64_t kernel_launches;      /* kernels + stream memory operations enqueued by coop calls
+                                    (the host fetch's gather launches are in ut_get_stats)       */
+  uint64_t block_rows;           /* rows per ownership block                                     */
+  uint64_t region_bytes;         /* bytes of this rank's symmetric region                        */
+} ut_coop_stats;
+
+/* Fill *s (synchronises with the device for the device-side counters). */
+UT_API int ut_coop_get_stats(const ut_coop* c, ut_coop_stats* s);
+
+/* As ut_error_pos, for indices this rank dispatched: syncs `stream`, reports and clears the
+ * smallest bad position (-1 and UT_OK if none, UT_ERANGE otherwise). */
+UT_API int ut_coop_error_pos(const ut_coop* c, ut_stream_t stream, int64_t* first_bad);
+
+/* Ownership (host function, no CUDA call): the rank owning row id of a rows x row_bytes table
+ * split among `world` ranks, and its dense index in the owner's tag table (*local, may be NULL).
+ * Blocks of R = 2 MiB / row_bytes rows (one translation region; fewer when the table has under
+ * 64 blocks per rank, at least 1) go round-robin: owner = (id / R) mod world. UINT32_MAX for
+ * invalid arguments or an id outside [0, rows). */
+UT_API uint32_t ut_coop_owner(uint64_t rows, uint64_t row_bytes, int world, int64_t id,
+                              uint64_t* local);
+
+/* Release: waits for the device, unmaps the peers' regions, frees this rank's. NULL is a no-op.
+ * Every rank should release only after all ranks finished their last step. */
+UT_API int ut_coop_release(ut_coop* c);
+
 #ifdef __cplusplus
 }
 #endif

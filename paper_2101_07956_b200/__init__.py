@@ -30,7 +30,11 @@ ABI = ("ut_register", "ut_gather", "ut_gather_host", "ut_release", "ut_error_pos
        "ut_last_error", "ut_plan_name", "ut_plan_probe", "ut_set_plan", "ut_table_get_info",
        "ut_get_stats", "ut_create", "ut_graph_register", "ut_graph_set_option", "ut_sample",
        "ut_graph_release", "ut_mem_advise", "ut_gather_dn", "ut_sample_async",
-       "ut_sample_capacity", "ut_graph_launches")
+       "ut_sample_capacity", "ut_graph_launches", "ut_coop_create", "ut_coop_export",
+       "ut_coop_open", "ut_coop_dispatch", "ut_coop_fetch", "ut_coop_combine", "ut_coop_gather",
+       "ut_coop_get_stats", "ut_coop_error_pos", "ut_coop_owner", "ut_coop_release")
+
+UT_COOP_HANDLE_BYTES = 64
 
 UT_ALLOC = {"pinned": 0, "managed": 1, "vmm": 2}
 
@@ -53,6 +57,13 @@ class _Stats(ctypes.Structure):
     _fields_ = [("gathers", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
                 ("rows", ctypes.c_uint64), ("bytes", ctypes.c_uint64),
                 ("timed_launches", ctypes.c_uint64), ("gather_kernel_ms", ctypes.c_double)]
+
+
+class _CoopStats(ctypes.Structure):
+    _fields_ = [("steps", ctypes.c_uint64), ("requested_rows", ctypes.c_uint64),
+                ("owner_requests", ctypes.c_uint64), ("unique_rows_fetched", ctypes.c_uint64),
+                ("last_unique_rows", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
+                ("block_rows", ctypes.c_uint64), ("region_bytes", ctypes.c_uint64)]
 
 
 def _load():
@@ -102,6 +113,28 @@ def _load():
     L.ut_graph_release.argtypes = [vp]
     L.ut_get_stats.restype = ctypes.c_int
     L.ut_get_stats.argtypes = [vp, ctypes.POINTER(_Stats), ctypes.c_int]
+    L.ut_coop_create.restype = vp
+    L.ut_coop_create.argtypes = [vp, ctypes.c_int, ctypes.c_int, u64]
+    L.ut_coop_export.restype = ctypes.c_int
+    L.ut_coop_export.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint64)]
+    L.ut_coop_open.restype = ctypes.c_int
+    L.ut_coop_open.argtypes = [vp, vp]
+    L.ut_coop_dispatch.restype = ctypes.c_int
+    L.ut_coop_dispatch.argtypes = [vp, vp, u64, vp]
+    L.ut_coop_fetch.restype = ctypes.c_int
+    L.ut_coop_fetch.argtypes = [vp, vp]
+    L.ut_coop_combine.restype = ctypes.c_int
+    L.ut_coop_combine.argtypes = [vp, vp, vp]
+    L.ut_coop_gather.restype = ctypes.c_int
+    L.ut_coop_gather.argtypes = [vp, vp, u64, vp, vp]
+    L.ut_coop_get_stats.restype = ctypes.c_int
+    L.ut_coop_get_stats.argtypes = [vp, ctypes.POINTER(_CoopStats)]
+    L.ut_coop_error_pos.restype = ctypes.c_int
+    L.ut_coop_error_pos.argtypes = [vp, vp, i64p]
+    L.ut_coop_owner.restype = ctypes.c_uint32
+    L.ut_coop_owner.argtypes = [u64, u64, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(ctypes.c_uint64)]
+    L.ut_coop_release.restype = ctypes.c_int
+    L.ut_coop_release.argtypes = [vp]
     return L
 
 
@@ -237,6 +270,65 @@ def ut_graph_release(g: int) -> None:
     _check(_lib.ut_graph_release(g))
 
 
+def ut_coop_create(t: int, world: int, rank: int, max_n: int) -> int:
+    h = _lib.ut_coop_create(t, world, rank, max_n)
+    if not h:
+        code, msg = last_error()
+        raise UTError(code, msg)
+    return h
+
+
+def ut_coop_export(c: int) -> bytes:
+    buf = ctypes.create_string_buffer(UT_COOP_HANDLE_BYTES)
+    _check(_lib.ut_coop_export(c, buf, None))
+    return buf.raw
+
+
+def ut_coop_open(c: int, handles: bytes) -> None:
+    _check(_lib.ut_coop_open(c, handles))
+
+
+def ut_coop_dispatch(c: int, idx_dev: int, n: int, stream: int = 0) -> None:
+    _check(_lib.ut_coop_dispatch(c, idx_dev, n, stream))
+
+
+def ut_coop_fetch(c: int, stream: int = 0) -> None:
+    _check(_lib.ut_coop_fetch(c, stream))
+
+
+def ut_coop_combine(c: int, out_dev: int, stream: int = 0) -> None:
+    _check(_lib.ut_coop_combine(c, out_dev, stream))
+
+
+def ut_coop_gather(c: int, idx_dev: int, n: int, out_dev: int, stream: int = 0) -> None:
+    _check(_lib.ut_coop_gather(c, idx_dev, n, out_dev, stream))
+
+
+def ut_coop_get_stats(c: int) -> dict:
+    st = _CoopStats()
+    _check(_lib.ut_coop_get_stats(c, ctypes.byref(st)))
+    return {k: getattr(st, k) for k, _ in _CoopStats._fields_}
+
+
+def ut_coop_error_pos(c: int, stream: int = 0) -> int:
+    v = ctypes.c_int64(-1)
+    rc = _lib.ut_coop_error_pos(c, stream, ctypes.byref(v))
+    if rc not in (UT_OK, UT_ERANGE):
+        _check(rc)
+    return int(v.value)
+
+
+def ut_coop_owner(rows: int, row_bytes: int, world: int, row_id: int) -> tuple[int, int]:
+    """(owner rank, local index) of a row; (2**32 - 1, 0) for invalid arguments."""
+    loc = ctypes.c_uint64(0)
+    o = _lib.ut_coop_owner(rows, row_bytes, world, row_id, ctypes.byref(loc))
+    return int(o), int(loc.value)
+
+
+def ut_coop_release(c: int) -> None:
+    _check(_lib.ut_coop_release(c))
+
+
 # ---- convenience ----------------------------------------------------------------------------
 def _stream_handle(stream) -> int:
     import torch
@@ -348,6 +440,88 @@ class Table:
     def close(self) -> None:
         if getattr(self, "handle", None):
             ut_release(self.handle)
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Coop:
+    """One rank's side of a cooperative gather: the ranks of
+    `group` (a torch.distributed process group, used only to move the IPC handles and, with
+    sync="host", for the barriers between phases) gather their own index lists from `table`;
+    rows requested by several ranks are fetched from host memory once, by their owner.
+
+    sync="device": ut_coop_gather (phases ordered by flag words in peer memory, no host sync);
+    sync="host": dispatch / fetch / combine with a stream sync and a group barrier between."""
+
+    def __init__(self, table: Table, max_n: int, group=None, rank: int | None = None,
+                 world: int | None = None, sync: str = "device"):
+        import torch.distributed as dist
+        if world is None:
+            world = dist.get_world_size(group) if dist.is_initialized() else 1
+        if rank is None:
+            rank = dist.get_rank(group) if dist.is_initialized() else 0
+        assert sync in ("device", "host")
+        self.table, self.world, self.rank, self.sync, self.group = table, world, rank, sync, group
+        self.max_n = int(max_n)
+        self.handle = ut_coop_create(table.handle, world, rank, self.max_n)
+        if world > 1:
+            mine = ut_coop_export(self.handle)
+            allh = [None] * world
+            dist.all_gather_object(allh, mine, group=group)
+            ut_coop_open(self.handle, b"".join(allh))
+            dist.barrier(group=group)
+
+    def _barrier(self, stream) -> None:
+        import torch
+        import torch.distributed as dist
+        s = torch.cuda.current_stream() if stream is None else stream
+        s.synchronize()
+        if self.world > 1:
+            dist.barrier(group=self.group)
+
+    def gather(self, idx, out=None, stream=None):
+        """out[i] = table row idx[i] (uint8 [n, row_bytes] CUDA tensor); every rank calls it."""
+        import torch
+        assert idx.is_cuda and idx.dtype == torch.int64 and idx.is_contiguous()
+        n = idx.numel()
+        rb = self.table.row_bytes
+        if out is None:
+            out = torch.empty((n, rb), dtype=torch.uint8, device=idx.device)
+        else:
+            assert out.is_cuda and out.is_contiguous() and out.numel() * out.element_size() >= n * rb
+        sh = _stream_handle(stream)
+        if self.sync == "device":
+            ut_coop_gather(self.handle, idx.data_ptr(), n, out.data_ptr(), sh)
+            return out
+        ut_coop_dispatch(self.handle, idx.data_ptr(), n, sh)
+        self._barrier(stream)
+        ut_coop_fetch(self.handle, sh)
+        self._barrier(stream)
+        ut_coop_combine(self.handle, out.data_ptr(), sh)
+        return out
+
+    __getitem__ = gather
+
+    def stats(self) -> dict:
+        return ut_coop_get_stats(self.handle)
+
+    def error_pos(self, stream=None) -> int:
+        return ut_coop_error_pos(self.handle, _stream_handle(stream))
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            ut_coop_release(self.handle)
             self.handle = None
 
     def __enter__(self):
