@@ -70,7 +70,8 @@ def make_index_lists(spec: dict, rank: int, world: int, count: int, seed: int,
         return [workloads.uniform_idx(spec["n"], spec["rows"], seed=seed + 1000003 * (b * world + rank))
                 for b in range(count)]
     rev = bool(spec.get("reverse_fanouts"))
-    jobs = [(spec["config"], seed, b, rank, world, rev) for b in range(count)]
+    edges = spec["edges"] if spec["edges"] != graphsage.CONFIGS[spec["config"]]["n_edges"] else None
+    jobs = [(spec["config"], seed, b, rank, world, rev, edges) for b in range(count)]
     if procs > 1 and count > 1:
         with mp.get_context("spawn").Pool(min(procs, count)) as pool:
             return pool.map(graphsage.minibatch_job, jobs)
@@ -264,7 +265,7 @@ def ncu_traffic(workload: str, plan: str, args) -> dict:
             rec = json.load(f).get(workload)
     except (OSError, ValueError):
         rec = None
-    if not rec or rec.get("plan") != plan or args.plan or args.sample != "cpu":
+    if not rec or rec.get("plan") != plan or args.plan or args.sample != "cpu" or args.coop != "off":
         return {"traffic": None}
     return {"traffic": rec["hbm_bytes_per_launch"],
             "traffic_detail": {k: rec[k] for k in ("hbm_bytes_per_launch", "hbm_write_bytes_per_launch",
@@ -415,6 +416,15 @@ def run_ut(args, spec, dist):
             table.set_plan(p)
     rb = spec["row_bytes"]
     stream = torch.cuda.current_stream()
+    coop = None
+    if args.coop != "off":
+        # cooperative gather: rows sampled by several ranks in a step are
+        # fetched from host memory once, by their owner, and exchanged through device memory
+        assert args.sample == "cpu", "--coop takes CPU-sampled index lists"
+        coop_max = int(dist.allreduce([float(max(l.size for l in lists))], "max")[0])
+        coop = ut.Coop(table, coop_max, rank=rank, world=world, sync=args.coop)
+    gather = (lambda l, o, st=None: coop.gather(l, out=o, stream=st)) if coop is not None else \
+             (lambda l, o, st=None: table.gather(l, out=o, stream=st))
     sampler = None
     if args.sample == "gpu":
         sampler = GpuSampling(spec, rank, world, count, seed, ut, torch, args.graph_indptr,
@@ -441,9 +451,10 @@ def run_ut(args, spec, dist):
         import oracle
         l = lists[0]
         want, bad = oracle.gather(hb.addr, spec["rows"], rb, l)
-        table.gather(idx_dev[0], out=out[: l.size * rb])
+        gather(idx_dev[0], out[: l.size * rb])
         got = out[: l.size * rb].cpu().numpy()
-        parity = bool(got.tobytes() == want.tobytes()) and table.error_pos() == bad
+        parity = bool(got.tobytes() == want.tobytes()) and \
+            (coop.error_pos() if coop is not None else table.error_pos()) == bad
         if not parity:
             raise SystemExit(f"rank {rank}: parity failure on minibatch 0")
 
@@ -455,13 +466,14 @@ def run_ut(args, spec, dist):
             sampler.step(s, table, out)
             continue
         l = idx_dev[s % count]
-        table.gather(l, out=out[: l.numel() * rb])
+        gather(l, out[: l.numel() * rb])
     torch.cuda.synchronize()
     if sampler is not None and sampler.mode != "sync":
         sampler.device_rows()          # drop the warm-up counts
 
     table.set_plan("timing=on")
     table.stats(reset=True)
+    coop0 = coop.stats() if coop is not None else None
     if sampler is not None:
         sampler.mark()
     evs = []
@@ -486,7 +498,7 @@ def run_ut(args, spec, dist):
             nbytes += sampler.step(args.warmup + s, table, out) * rb
         else:
             l = idx_dev[(args.warmup + s) % count]
-            table.gather(l, out=out[: l.numel() * rb], stream=stream)
+            gather(l, out[: l.numel() * rb], stream)
             nbytes += l.numel() * rb
         e1.record(stream)
         evs.append((e0, e1))
@@ -502,6 +514,22 @@ def run_ut(args, spec, dist):
     dev_ms = evs[0] if (sampler is not None and args.pipeline) else sum(a.elapsed_time(b) for a, b in evs)
 
     own_launches = st["kernel_launches"]
+    coop_block = None
+    if coop is not None:
+        c1 = coop.stats()
+        own_launches += c1["kernel_launches"] - coop0["kernel_launches"]
+        req = c1["requested_rows"] - coop0["requested_rows"]
+        uniq = c1["unique_rows_fetched"] - coop0["unique_rows_fetched"]
+        req_all, uniq_all = dist.allreduce([float(req), float(uniq)], "sum")
+        coop_block = {"sync": args.coop, "ranks": world,
+                      "requested_rows_per_step_all_ranks": round(req_all / args.steps, 1),
+                      "host_rows_per_step_all_ranks": round(uniq_all / args.steps, 1),
+                      "host_bytes_fraction": round(uniq_all / max(1.0, req_all), 4),
+                      "this_rank_fetch_rows_per_step": round(uniq / args.steps, 1),
+                      "block_rows": c1["block_rows"], "region_bytes": c1["region_bytes"],
+                      "note": "value counts useful rows (n*rb per rank); the host link moved "
+                              "host_bytes_fraction of them; roofline.achieved is host-fetched "
+                              "bytes / fetch-kernel time"}
     if sampler is not None:
         own_launches += sampler.timed_launches(args.steps)
     value, max_dev_ms, max_wall, launches = box_throughput(dist, nbytes, dev_ms, wall,
@@ -509,11 +537,13 @@ def run_ut(args, spec, dist):
     per_gpu = nbytes / (dev_ms / 1e3) / 1e9
     kern_ms = st["gather_kernel_ms"] / max(1, st["timed_launches"])
     kern_bytes = nbytes / max(1, st["timed_launches"])
+    if coop is not None:    # the gather kernels fetch the owners' unique rows only
+        kern_bytes = (c1["unique_rows_fetched"] - coop0["unique_rows_fetched"]) * rb / max(1, st["timed_launches"])
     achieved = kern_bytes / (kern_ms / 1e3) / 1e9 if kern_ms > 0 else None   # None: graph replay
 
     # end to end: host idx in (pinned), host rows out (pinned), through ut_gather_host
     e2e = None
-    if not args.no_e2e and sampler is None:
+    if not args.no_e2e and sampler is None and coop is None:
         idx_host = [torch.from_numpy(x).pin_memory() for x in lists]
         out_host = torch.empty(max_n * rb, dtype=torch.uint8, pin_memory=True)
         for s in range(min(2, count)):
@@ -617,9 +647,13 @@ def run_ut(args, spec, dist):
             "sampling": sampler.report(args.steps) if sampler is not None else None,
             "ranks_per_gpu": max(1, world // max(1, torch.cuda.device_count())),
             "parity_checked": parity, "register_s": round(reg_s, 3), "allreduce_smoke": ar,
+            "coop": coop_block,
             "wall_ms_per_step": round(max_wall / args.steps * 1e3, 3),
         }
         print(json.dumps(line), flush=True)
+    dist.barrier()
+    if coop is not None:
+        coop.close()
     table.close()
     dist.barrier()
     if world > 1 and rank == 0:
@@ -898,6 +932,11 @@ def main(argv=None):
     ap.add_argument("--no-check", dest="check", action="store_false")
     ap.add_argument("--backend", default="nccl", help="process-group backend at N > 1")
     ap.add_argument("--presort", action="store_true", help="experiment: sort index lists on the host")
+    ap.add_argument("--graph-edges", type=int, default=0,
+                    help="override Table 4's edge count of a GraphSAGE config (e.g. reddit 114600000)")
+    ap.add_argument("--coop", default="off", choices=["off", "device", "host"],
+                    help="cooperative gather across ranks (ut_coop; DESIGN.md §10d): phases "
+                         "synchronised on the device or by host barriers")
     ap.add_argument("--alloc", default="auto", choices=["auto", "register", "pinned", "managed", "vmm"],
                     help="table memory: caller mmap + ut_register, or ut_create(kind); auto = "
                          "managed for one rank and a table > 1 GiB, else register")
@@ -923,6 +962,8 @@ def main(argv=None):
     if args.reverse_fanouts and spec["kind"] == "graphsage":
         spec["reverse_fanouts"] = True          # DGL's order: the last fanout at the seeds (c15)
         spec["fanouts"] = list(reversed(spec["fanouts"]))
+    if args.graph_edges and spec["kind"] == "graphsage":
+        spec["edges"] = args.graph_edges        # E sensitivity (reading c17)
     dist = Dist()
     try:
         if args.impl == "reference":

@@ -12,9 +12,12 @@ Low level (same names and arguments as the C ABI, raw addresses and ints):
     ut_release(handle), ut_error_pos(handle, stream_handle) -> int, ut_get_stats(handle),
     ut_plan_name(handle), ut_set_plan(handle, name), ut_plan_probe(base, rows, rb, out),
     ut_table_get_info(handle) -> dict
+    ut_coop_create / _export / _open / _dispatch / _fetch / _combine / _gather / _get_stats /
+    _error_pos / _owner / _release (the cooperative multi-rank gather)
 
 High level: ``Table`` — the paper's unified tensor, ``Table(features)[gpu_idx]`` being
-``unified_tensor[gpu_tensor]`` (PAPER.md:377).
+``unified_tensor[gpu_tensor]``; ``Coop`` — one rank's side of the cooperative
+gather (rows requested by several ranks cross the host link once); ``Graph`` — GPU sampling.
 """
 from __future__ import annotations
 

@@ -170,14 +170,18 @@ CONFIGS = {
 }
 
 
-def sampler_for(config: str, seed: int = 1, reverse_fanouts: bool = False) -> GraphSageSampler:
+def sampler_for(config: str, seed: int = 1, reverse_fanouts: bool = False,
+                edges: int | None = None) -> GraphSageSampler:
+    """The config's sampler; `edges` overrides Table 4's E (reddit's E = 114.6M
+    sensitivity run, the paper does not say whether its E counts directed edges)."""
     c = CONFIGS[config]
-    g = ChungLuGraph(c["n_nodes"], c["n_edges"], seed=seed)
+    g = ChungLuGraph(c["n_nodes"], edges or c["n_edges"], seed=seed)
     return GraphSageSampler(g, c["batch"], c["fanouts"], seed=seed + 6,
                             reverse_fanouts=reverse_fanouts)
 
 
 def minibatch_job(args) -> np.ndarray:
-    """Picklable worker: (config, seed, batch, rank, world, reverse) -> index list."""
-    config, seed, batch, rank, world, reverse = args
-    return sampler_for(config, seed=seed, reverse_fanouts=reverse).minibatch(batch, rank, world)
+    """Picklable worker: (config, seed, batch, rank, world, reverse[, edges]) -> index list."""
+    config, seed, batch, rank, world, reverse = args[:6]
+    edges = args[6] if len(args) > 6 else None
+    return sampler_for(config, seed=seed, reverse_fanouts=reverse, edges=edges).minibatch(batch, rank, world)
