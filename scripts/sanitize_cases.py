@@ -1,5 +1,6 @@
 """Tiny cases for compute-sanitizer (memcheck / racecheck / synccheck): every kernel family,
-the reorder stage, the TMA bulk plan, the paper's kernels, host end-to-end and GPU sampling."""
+the reorder stage, the TMA bulk plan, the paper's kernels, host end-to-end, GPU sampling and
+the cooperative gather (one rank: dispatch, dedup, host fetch, combine)."""
 import os
 import sys
 
@@ -46,5 +47,23 @@ with ut.Graph(g.indptr_addr, g.indices_addr, g.n_nodes, g.n_edges, keep=g) as gr
     got = gr.sample(torch.from_numpy(seeds).cuda(), [5, 3], 11).cpu().numpy()
     want = oracle.sample(g.indptr_addr, g.indices_addr, g.n_nodes, seeds, [5, 3], 11)
     bad += not np.array_equal(got, want)
+for rb, off in [(68, 3), (400, 0), (2408, 8), (13, 1)]:
+    rows = 2000
+    hb = workloads.HostBuffer(rows * rb, kind="guarded")
+    workloads.fill_table(hb.addr, rows, rb, rb + 1)
+    idx = workloads.uniform_idx(900, rows, rb + 2)
+    idx[:3] = [0, rows - 1, 0]
+    idx[7] = rows                      # out of range: zero row + recorded position
+    want, want_bad = oracle.gather(hb.addr, rows, rb, idx)
+    with ut.Table(hb.addr, rows, rb) as t:
+        for sync in ("device", "host"):
+            with ut.Coop(t, 1000, world=1, rank=0, sync=sync) as c:
+                for _ in range(3):     # both buffer parities
+                    buf = torch.zeros(900 * rb + 16, dtype=torch.uint8, device="cuda")
+                    c.gather(torch.from_numpy(idx).cuda(), out=buf[off: off + 900 * rb])
+                    got = buf[off: off + 900 * rb].cpu().numpy()
+                    bad += got.tobytes() != want.tobytes()
+                    bad += c.error_pos() != want_bad
+    hb.close()
 torch.cuda.synchronize()
 print("SANITIZE-CASES-DONE bad=%d" % bad)
