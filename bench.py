@@ -624,6 +624,9 @@ def run_ut(args, spec, dist):
             "config": cfg,
             "per_gpu_gbs": round(per_gpu, 3),
             "transferred_gbs_sector_floor": round(value * sect_ratio, 3) if sect_ratio else None,
+            # rows < 128 B are bound by the link's request rate, not bytes
+            "line_requests_per_s": (round(cfg["line_requests_per_step"] * world / (max_dev_ms / args.steps / 1e3))
+                                    if cfg.get("line_requests_per_step") else None),
             "h2d_memcpy_gbs": round(link, 3),
             "h2d_memcpy_concurrent_gbs": round(link_sum, 3),
             "host_dram_read_gbs": dram,

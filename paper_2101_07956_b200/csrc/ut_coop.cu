@@ -169,26 +169,43 @@ __global__ void k_dedup(FetchArgs f) {
     if (PASS == 1) {
       if (live) atomicMax(&f.tag[l], ((unsigned long long)f.epoch << 32) | (uint32_t)~(uint32_t)e);
     } else if (PASS == 2) {
+      // winners take consecutive staging slots: one atomicAdd per block and loop iteration
+      __shared__ uint32_t warp_tot[32];
+      __shared__ unsigned long long block_base;
       const bool win = live && (uint32_t)~(uint32_t)f.tag[l] == (uint32_t)e;
       const uint32_t wm = __ballot_sync(kFull, win);
-      const uint32_t lane = lane_id();
-      unsigned long long b = 0;
-      if (wm && lane == (uint32_t)(__ffs(wm) - 1)) b = atomicAdd(&f.u[0], (unsigned long long)__popc(wm));
-      b = __shfl_sync(kFull, b, __ffs(wm ? wm : 1u) - 1);
+      const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      if (lane == 0) warp_tot[warp] = __popc(wm);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t tot = 0;
+        for (uint32_t k = 0; k < nw; ++k) {
+          const uint32_t c = warp_tot[k];
+          warp_tot[k] = tot;                 // exclusive prefix over the block's warps
+          tot += c;
+        }
+        block_base = tot ? atomicAdd(&f.u[0], (unsigned long long)tot) : 0ull;
+      }
+      __syncthreads();
       if (win) {
-        const uint64_t s = b + __popc(wm & ((1u << lane) - 1));
+        const uint64_t s = block_base + warp_tot[warp] + __popc(wm & ((1u << lane) - 1));
         f.uniq[s] = id;
         f.wslot[e] = (uint32_t)s;
       }
-      const uint32_t lm = __ballot_sync(kFull, live);
-      if (lane == 0 && lm) atomicAdd(&f.u[2], (unsigned long long)__popc(lm));
+      __syncthreads();                       // warp_tot / block_base reused next iteration
     } else {
       if (live) f.slot_of[e] = f.wslot[~(uint32_t)f.tag[l]];
     }
   }
 }
 
-__global__ void k_unique_total(unsigned long long* u) { u[1] += u[0]; }
+// all-time counters: unique rows fetched, requests received (sum of the sources' counts)
+__global__ void k_unique_total(unsigned long long* u, const uint64_t* count, uint32_t world) {
+  uint64_t req = 0;
+  for (uint32_t q = 0; q < world; ++q) req += count[q];
+  u[1] += u[0];
+  u[2] += req;
+}
 
 // ---- combine (requester side) ---------------------------------------------------------------
 // out[i] = staging row slot_of[rank][slot] of owner o, copied with W-byte words (W = the widest
@@ -443,7 +460,7 @@ int ut_coop_fetch(ut_coop* c, ut_stream_t stream) {
   k_dedup<1><<<grid(c, E), 256, 0, st>>>(f);
   k_dedup<2><<<grid(c, E), 256, 0, st>>>(f);
   k_dedup<3><<<grid(c, E), 256, 0, st>>>(f);
-  k_unique_total<<<1, 1, 0, st>>>(c->u);
+  k_unique_total<<<1, 1, 0, st>>>(c->u, f.count, (uint32_t)c->world);
   c->launches += 4;
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_err(e, "coop dedup");

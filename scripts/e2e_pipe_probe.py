@@ -57,11 +57,13 @@ def main():
             torch.cuda.synchronize(); sec += time.perf_counter() - t0; nb += ih.numel() * rb
         return round(nb / sec / 1e9, 2)
 
+    print(json.dumps({"cfg": cfg, "path": "direct-first", "e2e": rate(direct)}), flush=True)
     # parity of the pipe path
     pipe(idx_h[0], 16384)
     want, _ = __import__("oracle").gather(hb.addr, rows, rb, lists[0])
     assert out_h[: lists[0].size * rb].numpy().tobytes() == want.tobytes()
     print(json.dumps({"cfg": cfg, "path": "direct", "e2e": rate(direct)}), flush=True)
+    print(json.dumps({"cfg": cfg, "path": "direct-again", "e2e": rate(direct)}), flush=True)
     for cr in (4096, 16384, 65536):
         print(json.dumps({"cfg": cfg, "path": "pipe-smcopy", "chunk_rows": cr, "e2e": rate(pipe, cr)}), flush=True)
 

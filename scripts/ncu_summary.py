@@ -97,7 +97,7 @@ def main():
     a = ap.parse_args()
     if a.traffic:
         return traffic(a.traffic, a.bench, a.out)
-    h, u, vals = raw(a.rep)
+    h, u, vals = raw(a.rep) if a.rep else ([], [], [])
     for v in vals:
         name = v[h.index("Kernel Name")]
         print(f"kernel: {name}")
