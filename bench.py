@@ -578,6 +578,9 @@ def run_ut(args, spec, dist):
             probe.copy_(res[:8].view(torch.int64), non_blocking=False)
             f_sec += time.perf_counter() - t1
             f_bytes += ih.numel() * rb
+            if os.environ.get("UT_BENCH_DEBUG"):
+                print(f"to_hbm step {s}: {(time.perf_counter() - t1) * 1e3:.3f} ms, n={ih.numel()}",
+                      file=sys.stderr)
         mx = dist.allreduce([f_sec], "max")[0]
         f_tot = dist.allreduce([float(f_bytes)], "sum")[0]
         e2e["to_hbm"] = {"value": round(f_tot / mx / 1e9, 3), "unit": "GB/s",

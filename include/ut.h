@@ -192,6 +192,9 @@ UT_API const char* ut_plan_probe(uint64_t base, uint64_t rows, uint64_t row_byte
  * "timing=on|off" brackets each gather-kernel launch with CUDA events (see ut_get_stats).
  * "runs=on|off" (default off): for 16-B aligned tables, sort the rows exactly and copy runs of
  * table-adjacent rows with one warp so shared boundary lines are requested once.
+ * "stage=on|off|auto" (auto = off): ut_gather_host's direct path gathers tiles of consecutive
+ * output rows into shared memory and writes each tile's span with whole-line stores (k_staged;
+ * an A/B knob — measured no gain).
  * "conc=auto|dense|sparse" picks the launch shape: dense = every SM full of warps; sparse = a
  * quarter of the SMs, one row-step per warp (fewer translation pages in flight); auto = sparse
  * for reordered gathers from tables > 1 GiB.

@@ -278,6 +278,7 @@ struct ut_table {
   bool timing = false;                  // ut_set_plan "timing=on"
   int conc = -1;                        // launch shape: -1 auto, 0 dense, 1 sparse ("conc=...")
   int runs = -1;                        // run merge: -1 auto, 0 off, 1 on ("runs=...")
+  int stage = -1;                       // host-output tile staging: -1 auto (= off), 0 off, 1 on ("stage=...")
   std::mutex mu;
   DevState dev[kMaxDev];
 };
@@ -516,6 +517,42 @@ int bucket_shift(uint64_t table_bytes, uint64_t rb) {
 }
 
 bool want_runs(const ut_table* t, const Plan& p, uint64_t n);
+template <typename F>
+cudaError_t timed(const ut_table* t, DevState* s, cudaStream_t st, F&& fn);
+
+// Host-output tile staging (k_staged, opt-in "stage=on"): for ut_gather_host's direct path, when
+// base, rb and out share a 4-B (or wider) alignment and 16 B <= rb <= 8 KiB. Measured no gain:
+// whole-line writes leave host->host e2e unchanged at 400-B rows (29.9 vs 29.7 GB/s) and lose at
+// 512 B (37.8 vs 39.5) and 2408 B (32.9 vs 34.7) to the tile barriers
+// (profiles/r1d/e2e_rb_stage.jsonl), so "auto" keeps per-row stores.
+int stage_width(const ut_table* t, uint64_t out) {
+  const uint64_t m = (uint64_t)t->host | t->rb | out;
+  return (m & 15) == 0 ? 16 : (m & 7) == 0 ? 8 : (m & 3) == 0 ? 4 : 0;
+}
+
+bool want_stage(const ut_table* t, uint64_t out, const Plan& p) {
+  if (t->stage == 0 || t->rb < 16 || t->rb > 8192 || stage_width(t, out) == 0) return false;
+  (void)p;
+  return t->stage == 1;
+}
+
+cudaError_t launch_staged(const ut_table* t, DevState* s, cudaStream_t st, const ut::GatherArgs& a) {
+  const uint32_t tile_rows = (uint32_t)std::max<uint64_t>(
+      1, std::min<uint64_t>(ut::kStageMaxRows, ut::kStageBytes / t->rb));
+  const uint64_t ntiles = (a.n + tile_rows - 1) / tile_rows;
+  auto go = [&](auto k) {
+    const int per_sm = occupancy((const void*)k);
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)s->sms * per_sm, ntiles));
+    k<<<grid, 256, 0, st>>>(a, tile_rows);
+    return cudaGetLastError();
+  };
+  switch (stage_width(t, a.out)) {
+    case 16: return go(ut::k_staged<uint4, 4>);
+    case 8: return go(ut::k_staged<uint2, 4>);
+    default: return go(ut::k_staged<uint32_t, 4>);
+  }
+}
+
 int gather_runs(const ut_table* t, DevState* s, const Plan& p, const ut::GatherArgs& a, cudaStream_t st);
 
 int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n, void* out_dev,
@@ -530,6 +567,11 @@ int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n
   s->bytes += n * t->rb;
   const bool runs = want_runs(t, p, n);
   if (!runs && (!want_reorder(t, n) || p.kind == P_PAPER_NAIVE || p.kind == P_PAPER_SHIFT)) {
+    if (host_out && want_stage(t, (uint64_t)out_dev, p)) {
+      e = timed(t, s, st, [&] { return launch_staged(t, s, st, a); });
+      if (e != cudaSuccess) return cuda_err(e, "staged gather");
+      return UT_OK;
+    }
     e = timed_launch<false>(t, s, p, st, a, host_out);
     if (e != cudaSuccess) return cuda_err(e, plan_name(p));
     return UT_OK;
@@ -1162,6 +1204,14 @@ int ut_set_plan(ut_table* t, const char* name) {
     else if (!strcmp(v, "on")) t->runs = 1;
     else if (!strcmp(v, "off")) t->runs = 0;
     else return set_err(UT_EINVAL, "runs must be auto|on|off, got '%s'", v);
+    return UT_OK;
+  }
+  if (!strncmp(name, "stage=", 6)) {
+    const char* v = name + 6;
+    if (!strcmp(v, "auto")) t->stage = -1;
+    else if (!strcmp(v, "on")) t->stage = 1;
+    else if (!strcmp(v, "off")) t->stage = 0;
+    else return set_err(UT_EINVAL, "stage must be auto|on|off, got '%s'", v);
     return UT_OK;
   }
   if (!strncmp(name, "conc=", 5)) {

@@ -347,6 +347,97 @@ __global__ void __launch_bounds__(256, UT_MINB) k_multi(GatherArgs a_) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// staged<T>: output rows in mapped HOST memory (ut_gather_host's direct path). A block owns a
+// tile of consecutive output rows: it reads the tile's rows from the table into shared memory
+// (flattened over the tile's W-byte chunks, U chunks per thread in flight), then writes the tile's
+// contiguous output span with coalesced W-byte stores, so the write side of the link sees whole
+// 128-B lines except at tile edges instead of two partial lines per row. The hypothesis (rows of
+// 400 B reach 29.7 GB/s host->host vs 36.6-39.9 for rows that are whole lines) did not hold: the
+// gap is on the read side, and staging gains nothing (opt-in only, "stage=on").
+// Requires base, rb and out to be W-aligned (W = sizeof(T)); the tile is <= kStageBytes.
+constexpr int kStageBytes = 16384;
+constexpr int kStageMaxRows = 1024;
+
+template <typename T>
+__device__ __forceinline__ T ld_table_w(uint64_t a);
+template <>
+__device__ __forceinline__ uint4 ld_table_w<uint4>(uint64_t a) {
+  const V4 v = ld_table16(a);
+  return make_uint4(v.x, v.y, v.z, v.w);
+}
+template <>
+__device__ __forceinline__ uint2 ld_table_w<uint2>(uint64_t a) {
+  uint2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(a));
+  return v;
+}
+template <>
+__device__ __forceinline__ uint32_t ld_table_w<uint32_t>(uint64_t a) {
+  uint32_t v;
+  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(a));
+  return v;
+}
+
+// The tile sits in shared memory at the output span's offset within its first 128-B line, so
+// shared 16-B chunk g is the output's 16-B chunk g counted from that line: every warp store
+// instruction then covers 4 whole aligned lines, and only the tile's two edge lines are partial.
+template <typename T, int U>
+__global__ void __launch_bounds__(256) k_staged(GatherArgs a_, uint32_t tile_rows) {
+  const GatherArgs a = with_dev_n(a_);
+  __shared__ __align__(128) uint8_t tile[kStageBytes + 128];
+  __shared__ uint64_t src[kStageMaxRows];          // per tile row: source address, or ~0 if bad
+  constexpr uint32_t W = sizeof(T);
+  const uint32_t cpr = (uint32_t)(a.rb / W);       // chunks per row
+  const uint64_t ntiles = (a.n + tile_rows - 1) / tile_rows;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint64_t r0 = t * tile_rows;
+    const uint32_t nr = (uint32_t)((a.n - r0) < tile_rows ? (a.n - r0) : tile_rows);
+    const uint64_t D0 = a.out + r0 * a.rb;
+    const uint32_t h = (uint32_t)(D0 & 127);       // a multiple of W
+    const uint32_t bytes = nr * (uint32_t)a.rb;
+    for (uint32_t k = threadIdx.x; k < nr; k += blockDim.x) {
+      const int64_t r = __ldg(a.idx + r0 + k);
+      const bool ok = (uint64_t)r < a.rows;
+      src[k] = ok ? a.tbase + (uint64_t)r * a.rb : ~0ull;
+      if (!ok) record_bad(a.err, r0 + k);
+    }
+    __syncthreads();
+    const uint32_t nch = nr * cpr;
+    T* tl = reinterpret_cast<T*>(tile + h);        // chunk f of the tile = row f / cpr, chunk f % cpr
+    for (uint32_t f0 = 0; f0 < nch; f0 += blockDim.x * U) {
+      T v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t f = f0 + u * blockDim.x + threadIdx.x;
+        v[u] = T{};
+        if (f < nch) {
+          const uint32_t row = f / cpr, c = f - row * cpr;
+          const uint64_t sa = src[row];
+          if (sa != ~0ull) v[u] = ld_table_w<T>(sa + (uint64_t)c * W);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t f = f0 + u * blockDim.x + threadIdx.x;
+        if (f < nch) tl[f] = v[u];
+      }
+    }
+    __syncthreads();
+    const uint64_t L0 = D0 - h;                    // the span's first 128-B line
+    const uint32_t G = (h + bytes + 15) / 16;
+    for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) {
+      const uint4 w = reinterpret_cast<const uint4*>(tile)[g];
+      const V4 v{w.x, w.y, w.z, w.w};
+      const uint32_t lo = 16 * g < h ? h - 16 * g : 0;
+      const uint32_t hi = h + bytes - 16 * g < 16 ? h + bytes - 16 * g : 16;
+      if (lo == 0 && hi == 16) st16(L0 + 16ull * g, v);
+      else st_partial(L0 + 16ull * g, v, (int)lo, (int)hi);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // bulk<U>: the row is fetched by the TMA unit (1-D cp.async.bulk global -> shared, completion on an
 // mbarrier) instead of by LDG, then stored to HBM from shared memory. Table base, rb and out
 // 16-B aligned, rb <= kBulkMaxRow. One warp per row-slot, U rows in flight per warp.

@@ -313,3 +313,32 @@ def test_concurrent_gathers_from_threads_and_streams():
         st = t.stats()
         assert st["gathers"] >= 30 and st["timed_launches"] <= st["gathers"]
     hb.close()
+
+
+@pytest.mark.parametrize("rb,base_off,out_off", [(400, 0, 0), (68, 0, 0), (2408, 0, 0), (16, 0, 0),
+                                                 (8192, 0, 0), (100, 4, 8), (400, 0, 4), (36, 2, 0)])
+@pytest.mark.parametrize("stage", ["on", "off"])
+def test_gather_host_staged_tiles(rb, base_off, out_off, stage):
+    """ut_gather_host's direct path with and without host-output tile staging (k_staged): tiles
+    of consecutive output rows, ragged last tile, out-of-range rows, any admissible alignment
+    (stage=on falls back to per-row stores when base/rb/out share no 4-B alignment)."""
+    rows = 50_000 if rb < 4096 else 3000
+    hb = workloads.HostBuffer(rows * rb, offset=base_off)
+    workloads.fill_table(hb.array(), rows, rb, rb)
+    n = 12_345
+    idx = workloads.uniform_idx(n, rows, rb + 1)
+    idx[:3] = [0, rows - 1, 0]
+    idx[1000] = -7
+    idx[n - 1] = rows
+    want, bad = oracle.gather(hb.addr, rows, rb, idx)
+    with ut.Table(hb.addr, rows, rb) as t:
+        t.set_plan(f"stage={stage}")
+        idx_h = torch.from_numpy(idx).pin_memory()
+        buf = torch.full((n * rb + out_off + 64,), SENT, dtype=torch.uint8, pin_memory=True)
+        out = buf[out_off:out_off + n * rb]
+        t.gather_host(idx_h, out_host=out)
+        got = buf.numpy()
+        assert got[out_off:out_off + n * rb].tobytes() == want.tobytes()
+        assert (got[:out_off] == SENT).all() and (got[out_off + n * rb:] == SENT).all()
+        assert t.error_pos() == bad == 1000
+    hb.close()
