@@ -384,8 +384,9 @@ typedef struct ut_coop_stats {
   uint64_t owner_requests;       /* requests this rank received as an owner (all sources)        */
   uint64_t unique_rows_fetched;  /* rows this rank fetched from host memory as an owner          */
   uint64_t last_unique_rows;     /* ... in the last fetch                                        */
-  uint64_t kernel_launches;      /* kernels + stream memory operations enqueued by coop calls
-                                    (the host fetch's gather launches are in ut_get_stats)       */
+  uint64_t kernel_launches;      /* kernels enqueued by coop calls (the host fetch's gather
+                                    kernels are counted by the table's ut_get_stats)             */
+  uint64_t stream_memops;        /* flag writes / waits of ut_coop_gather's device barriers      */
   uint64_t block_rows;           /* rows per ownership block                                     */
   uint64_t region_bytes;         /* bytes of this rank's symmetric region                        */
 } ut_coop_stats;

@@ -66,6 +66,7 @@ class _CoopStats(ctypes.Structure):
     _fields_ = [("steps", ctypes.c_uint64), ("requested_rows", ctypes.c_uint64),
                 ("owner_requests", ctypes.c_uint64), ("unique_rows_fetched", ctypes.c_uint64),
                 ("last_unique_rows", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
+                ("stream_memops", ctypes.c_uint64),
                 ("block_rows", ctypes.c_uint64), ("region_bytes", ctypes.c_uint64)]
 
 
@@ -479,10 +480,15 @@ class Coop:
         self.max_n = int(max_n)
         self.handle = ut_coop_create(table.handle, world, rank, self.max_n)
         if world > 1:
-            mine = ut_coop_export(self.handle)
+            # every rank must agree on the layout of the symmetric regions it is about to map
+            mine = (ut_coop_export(self.handle), (world, self.max_n, table.rows, table.row_bytes))
             allh = [None] * world
             dist.all_gather_object(allh, mine, group=group)
-            ut_coop_open(self.handle, b"".join(allh))
+            shapes = {h[1] for h in allh}
+            if len(shapes) != 1:
+                self.close()
+                raise UTError(UT_EINVAL, f"ranks disagree on (world, max_n, rows, row_bytes): {sorted(shapes)}")
+            ut_coop_open(self.handle, b"".join(h[0] for h in allh))
             dist.barrier(group=group)
 
     def _barrier(self, stream) -> None:

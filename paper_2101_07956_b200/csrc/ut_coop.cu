@@ -291,7 +291,7 @@ struct ut_coop {
   unsigned long long* err = nullptr;
   uint32_t epoch = 0;                        // steps dispatched so far
   uint64_t last_n = 0;
-  uint64_t steps = 0, requested = 0, launches = 0;
+  uint64_t steps = 0, requested = 0, launches = 0, memops = 0;
   PWrite write32 = nullptr;
   PWait wait32 = nullptr;
 };
@@ -318,7 +318,7 @@ int device_barrier(ut_coop* c, int b, cudaStream_t st) {
     if (c->wait32((CUstream)st, f, c->epoch, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
       return set_err(UT_ECUDA, "cuStreamWaitValue32 on rank %d failed", q);
   }
-  c->launches += 2 * (uint64_t)c->world;
+  c->memops += 2 * (uint64_t)c->world;
   return UT_OK;
 }
 
@@ -514,6 +514,7 @@ int ut_coop_get_stats(const ut_coop* c, ut_coop_stats* s) {
   s->unique_rows_fetched = u[1];
   s->last_unique_rows = u[0];
   s->kernel_launches = c->launches;
+  s->stream_memops = c->memops;
   s->block_rows = c->own.R;
   s->region_bytes = c->L.total;
   return UT_OK;
