@@ -442,21 +442,29 @@ def run_ut(args, spec, dist):
     sm_ceiling = sm_read_ceiling(torch, ut)
 
     # parity (outside timing): the first minibatch against the oracle, byte for byte
-    parity = None
+    parity, parity_lists = None, 0
     if args.check and sampler is not None:
-        parity = sampler.check(hb.addr, table, out)
+        parity, parity_lists = sampler.check(hb.addr, table, out), 1
         if not parity:
             raise SystemExit(f"rank {rank}: parity failure (GPU sampling + gather)")
     elif args.check:
+        # every distinct index list the run gathers is checked against the oracle
+        # (bytes), outside timing — all of them up to 16 GB of rows, else the first four
         import oracle
-        l = lists[0]
-        want, bad = oracle.gather(hb.addr, spec["rows"], rb, l)
-        gather(idx_dev[0], out[: l.size * rb])
-        got = out[: l.size * rb].cpu().numpy()
-        parity = bool(got.tobytes() == want.tobytes()) and \
-            (coop.error_pos() if coop is not None else table.error_pos()) == bad
-        if not parity:
-            raise SystemExit(f"rank {rank}: parity failure on minibatch 0")
+        total = sum(l.size for l in lists) * rb
+        n_check = len(lists) if total <= (16 << 30) else min(4, len(lists))
+        want_buf = np.empty(max_n * rb, dtype=np.uint8)
+        parity = True
+        for k in range(n_check):
+            l = lists[k]
+            bad = oracle.gather_into(hb.addr, spec["rows"], rb, l, want_buf)
+            gather(idx_dev[k], out[: l.size * rb])
+            got = out[: l.size * rb].cpu().numpy()
+            ok = bool(got.tobytes() == want_buf[: l.size * rb].tobytes()) and \
+                (coop.error_pos() if coop is not None else table.error_pos()) == bad
+            if not ok:
+                raise SystemExit(f"rank {rank}: parity failure on minibatch {k}")
+        parity_lists = n_check
 
     clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
@@ -652,7 +660,8 @@ def run_ut(args, spec, dist):
             "gpu_launches": n_launch, "clocks": clk,
             "sampling": sampler.report(args.steps) if sampler is not None else None,
             "ranks_per_gpu": max(1, world // max(1, torch.cuda.device_count())),
-            "parity_checked": parity, "register_s": round(reg_s, 3), "allreduce_smoke": ar,
+            "parity_checked": parity, "parity_lists_checked": parity_lists,
+            "register_s": round(reg_s, 3), "allreduce_smoke": ar,
             "coop": coop_block,
             "wall_ms_per_step": round(max_wall / args.steps * 1e3, 3),
         }
