@@ -416,20 +416,23 @@ def run_ut(args, spec, dist):
             table.set_plan(p)
     rb = spec["row_bytes"]
     stream = torch.cuda.current_stream()
-    coop = None
-    if args.coop != "off":
-        # cooperative gather (SURVEY NEXT-4 (ii)): rows sampled by several ranks in a step are
-        # fetched from host memory once, by their owner, and exchanged through device memory
-        assert args.sample == "cpu", "--coop takes CPU-sampled index lists"
-        coop_max = int(dist.allreduce([float(max(l.size for l in lists))], "max")[0])
-        coop = ut.Coop(table, coop_max, rank=rank, world=world, sync=args.coop)
-    gather = (lambda l, o, st=None: coop.gather(l, out=o, stream=st)) if coop is not None else \
-             (lambda l, o, st=None: table.gather(l, out=o, stream=st))
     sampler = None
     if args.sample == "gpu":
         sampler = GpuSampling(spec, rank, world, count, seed, ut, torch, args.graph_indptr,
                               "graph" if args.graph else "async" if args.async_sample else "sync")
         lists = sampler.node_lists_for_accounting()
+    coop = None
+    if args.coop != "off":
+        # cooperative gather (SURVEY NEXT-4 (ii)): rows sampled by several ranks in a step are
+        # fetched from host memory once, by their owner, and exchanged through device memory
+        assert sampler is None or sampler.mode == "sync", "--coop with --sample gpu: sync sampling only"
+        need = sampler.capacity() if sampler is not None else max(l.size for l in lists)
+        coop_max = int(dist.allreduce([float(need)], "max")[0])
+        coop = ut.Coop(table, coop_max, rank=rank, world=world, sync=args.coop)
+    gather = (lambda l, o, st=None: coop.gather(l, out=o, stream=st)) if coop is not None else \
+             (lambda l, o, st=None: table.gather(l, out=o, stream=st))
+    if sampler is not None and coop is not None:
+        sampler.gather_fn = gather
     idx_dev = [torch.from_numpy(l).to("cuda") for l in lists]
     max_n = max(l.size for l in lists)
     out = torch.empty(max_n * rb, dtype=torch.uint8, device="cuda")
@@ -713,6 +716,16 @@ class GpuSampling:
         self.cuda_graph = None
         self.graph_kernels = 0
         self._l_mark = 0
+        self.gather_fn = None      # --coop: the cooperative gather replaces table.gather (sync mode)
+
+    def capacity(self) -> int:
+        return self.nodes.numel()
+
+    def _gather(self, table, nodes, out_view):
+        if self.gather_fn is not None:
+            self.gather_fn(nodes, out_view)
+        else:
+            table.gather(nodes, out=out_view)
 
     def node_lists_for_accounting(self):
         """The minibatches' node lists, computed on the GPU once (for the traffic model and the
@@ -737,7 +750,7 @@ class GpuSampling:
             e1.record()
             self.mid.append((e0, e1))
             n = nodes.numel()
-            table.gather(nodes, out=out[: n * self.spec["row_bytes"]])
+            self._gather(table, nodes, out[: n * self.spec["row_bytes"]])
             self.rows += n
             return n
         self.seeds_buf.copy_(self.roots_dev[b])
@@ -830,7 +843,7 @@ class GpuSampling:
             return False
         rb = self.spec["row_bytes"]
         want, _ = oracle.gather(table_addr, self.spec["rows"], rb, want_nodes)
-        table.gather(got_nodes, out=out[: got_nodes.numel() * rb])
+        self._gather(table, got_nodes, out[: got_nodes.numel() * rb])
         return out[: got_nodes.numel() * rb].cpu().numpy().tobytes() == want.tobytes()
 
     def report(self, steps):
