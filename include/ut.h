@@ -374,7 +374,9 @@ UT_API int ut_coop_fetch(ut_coop* c, ut_stream_t stream);
 UT_API int ut_coop_combine(ut_coop* c, void* out_dev, ut_stream_t stream);
 
 /* The three phases with device-side barriers between them (every rank calls it for the step).
- * Returns UT_OK, UT_EINVAL, UT_ENOTSUP (no stream memory operations) or UT_ECUDA. */
+ * Returns UT_OK, UT_EINVAL, UT_ENOTSUP (no stream memory operations) or UT_ECUDA. On UT_EINVAL
+ * for n > max_n or a NULL buffer, the rank still took part in the step with n = 0 (its peers'
+ * device waits are satisfied); out_dev is untouched. */
 UT_API int ut_coop_gather(ut_coop* c, const int64_t* idx_dev, uint64_t n, void* out_dev,
                           ut_stream_t stream);
 

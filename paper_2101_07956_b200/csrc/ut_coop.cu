@@ -495,11 +495,24 @@ int ut_coop_combine(ut_coop* c, void* out_dev, ut_stream_t stream) {
 }
 
 int ut_coop_gather(ut_coop* c, const int64_t* idx_dev, uint64_t n, void* out_dev, ut_stream_t stream) {
+  if (!c) return set_err(UT_EINVAL, "coop is NULL");
+  // Bad arguments on one rank must not strand its peers at the device barriers: take part in
+  // the step with no rows, then report the error.
+  int bad = UT_OK;
+  if (n > c->cap) bad = set_err(UT_EINVAL, "n = %llu exceeds max_n = %llu", (unsigned long long)n,
+                                (unsigned long long)c->cap);
+  else if (n > 0 && (!idx_dev || !out_dev)) bad = set_err(UT_EINVAL, "idx_dev/out_dev is NULL");
+  if (bad != UT_OK) n = 0;
   int rc = ut_coop_dispatch(c, idx_dev, n, stream);
   if (rc == UT_OK && c->world > 1) rc = device_barrier(c, 0, (cudaStream_t)stream);
   if (rc == UT_OK) rc = ut_coop_fetch(c, stream);
   if (rc == UT_OK && c->world > 1) rc = device_barrier(c, 1, (cudaStream_t)stream);
   if (rc == UT_OK) rc = ut_coop_combine(c, out_dev, stream);
+  if (rc == UT_OK && bad != UT_OK) {
+    char msg[512];
+    ut_last_error(msg, sizeof msg);     // keep the argument error, not a later success
+    return set_err(bad, "%s (the step ran with n = 0 so the peers are not stranded)", msg);
+  }
   return rc;
 }
 

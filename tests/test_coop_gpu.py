@@ -133,12 +133,22 @@ def _worker(rank, world, port, cfg, q):
         ok, fetched = True, []
         with ut.Table(hb.addr, rows, rb) as t, ut.Coop(t, n, sync=sync) as c:
             prev = 0
-            for l in lists:
-                want, want_bad = oracle.gather(hb.addr, rows, rb, l)
-                out = c.gather(torch.from_numpy(l).cuda())
-                got = out.cpu().numpy().reshape(-1)
-                ok &= got.tobytes() == want.tobytes()
-                ok &= c.error_pos() == want_bad
+            for k, l in enumerate(lists):
+                if cfg.get("overflow_rank") == rank and k == 1:
+                    # n > max_n on one rank: it errors, but still takes part in the step with no
+                    # rows, so the other ranks' device waits complete
+                    try:
+                        c.gather(torch.zeros(n + 1, dtype=torch.int64, device="cuda"))
+                        ok = False
+                    except ut.UTError:
+                        pass
+                    lists[k] = np.array([], dtype=np.int64)
+                else:
+                    want, want_bad = oracle.gather(hb.addr, rows, rb, l)
+                    out = c.gather(torch.from_numpy(l).cuda())
+                    got = out.cpu().numpy().reshape(-1)
+                    ok &= got.tobytes() == want.tobytes()
+                    ok &= c.error_pos() == want_bad
                 u = c.stats()["unique_rows_fetched"]
                 fetched.append(u - prev)
                 prev = u
@@ -187,3 +197,8 @@ def test_processes_share_gpu(world, sync):
 def test_processes_unaligned_rows_and_errors(rb):
     _run_world(2, {"rows": 30_000 if rb < 1000 else 4000, "rb": rb, "n": 3000, "steps": 3,
                    "sync": "device", "bad": True, "empty_rank": 1})
+
+
+def test_processes_one_rank_bad_arguments_does_not_strand_peers():
+    _run_world(3, {"rows": 20_000, "rb": 400, "n": 4000, "steps": 3, "sync": "device",
+                   "overflow_rank": 1})
