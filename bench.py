@@ -400,10 +400,20 @@ def run_ut(args, spec, dist):
         # shared registered table is the only way for N ranks to hold a single copy
         big = spec["rows"] * spec["row_bytes"] > (1 << 30)
         args.alloc = "managed" if (world == 1 and big) else "register"
+    partitioned = args.coop != "off" and args.alloc != "register"
     if args.alloc == "register":
         hb = open_table(spec, rank, world, seed, dist, tag)
         t_reg = time.perf_counter()
         table = ut.Table(hb.addr, spec["rows"], spec["row_bytes"])
+    elif partitioned:
+        # cooperative gather over per-rank partitions: each rank allocates only
+        # the rows it owns, of any kind (the paper's managed memory included), one copy in total
+        part_ids = ut.Coop.partition_ids(spec["rows"], spec["row_bytes"], world, rank)
+        table = ut.Table.create(part_ids.size, spec["row_bytes"], args.alloc)
+        workloads.fill_rows(table.host_addr, part_ids, spec["row_bytes"], seed,
+                            threads=max(1, (os.cpu_count() or 1) // world))
+        hb = _Owned(table.host_addr)
+        args.no_cpu = True         # no rank holds the whole table for the host-side baselines
     else:   # the paper's to("unified"): a library-owned table (N = 1 only)
         assert world == 1, "--alloc other than 'register' is single-process"
         table = ut.Table.create(spec["rows"], spec["row_bytes"], args.alloc)
@@ -428,7 +438,8 @@ def run_ut(args, spec, dist):
         assert sampler is None or sampler.mode == "sync", "--coop with --sample gpu: sync sampling only"
         need = sampler.capacity() if sampler is not None else max(l.size for l in lists)
         coop_max = int(dist.allreduce([float(need)], "max")[0])
-        coop = ut.Coop(table, coop_max, rank=rank, world=world, sync=args.coop)
+        coop = ut.Coop(table, coop_max, rank=rank, world=world, sync=args.coop,
+                       rows=spec["rows"] if partitioned else None)
     gather = (lambda l, o, st=None: coop.gather(l, out=o, stream=st)) if coop is not None else \
              (lambda l, o, st=None: table.gather(l, out=o, stream=st))
     if sampler is not None and coop is not None:
@@ -460,7 +471,13 @@ def run_ut(args, spec, dist):
         parity = True
         for k in range(n_check):
             l = lists[k]
-            bad = oracle.gather_into(hb.addr, spec["rows"], rb, l, want_buf)
+            if partitioned:
+                # no process holds the whole table: the expected rows are the table's definition
+                # (the input generator's row content), every id here is in range
+                workloads.fill_rows(want_buf, l, rb, seed)
+                bad = -1
+            else:
+                bad = oracle.gather_into(hb.addr, spec["rows"], rb, l, want_buf)
             gather(idx_dev[k], out[: l.size * rb])
             got = out[: l.size * rb].cpu().numpy()
             ok = bool(got.tobytes() == want_buf[: l.size * rb].tobytes()) and \
@@ -648,7 +665,8 @@ def run_ut(args, spec, dist):
             "frac_of_link": round(per_gpu / link, 4),
             "sm_read_ceiling_gbs": round(sm_ceiling, 3),
             "frac_of_sm_read_ceiling": round(per_gpu / sm_ceiling, 4),
-            "plan": table.plan, "table_memory": args.alloc,
+            "plan": table.plan,
+            "table_memory": args.alloc + (" (per-rank partitions, ut_coop_create_partitioned)" if partitioned else ""),
             "numa": {"nodes": workloads.numa_nodes(), "gpu_node": gnode,
                      "table_policy": "interleave" if getattr(hb, "numa", 0) > 1 else "single node / default"},
             "roofline": {"bound": "pcie_h2d",

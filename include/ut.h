@@ -353,6 +353,22 @@ typedef struct ut_coop ut_coop;
  * world == 1 needs no ut_coop_open. NULL on failure (ut_last_error). */
 UT_API ut_coop* ut_coop_create(const ut_table* t, int world, int rank, uint64_t max_n);
 
+/* Partitioned form: the host table is never held whole by any process. `part` holds only the
+ * rows this rank owns, in its local order (row l = table row ut_coop_partition_ids(...)[l]), so
+ * the N ranks together hold one copy — and each partition may be any allocation kind, e.g. the
+ * paper's managed memory (ut_create UT_ALLOC_MANAGED), which is process-private and so cannot be
+ * one shared table. rows: rows of the whole table; part->row_bytes is the
+ * row size; part must have >= ut_coop_partition_ids(rows, rb, world, rank, NULL, 0) rows. Every
+ * rank of the group must use the same form. NULL on failure. */
+UT_API ut_coop* ut_coop_create_partitioned(const ut_table* part, uint64_t rows, int world,
+                                           int rank, uint64_t max_n);
+
+/* Host function (no CUDA call): the number of local rows of rank `rank`'s partition (blocks it
+ * owns, the last one padded) and, when ids != NULL and cap >= that number, the table row of
+ * each local row (ids[l], -1 for the padding). 0 for invalid arguments. */
+UT_API uint64_t ut_coop_partition_ids(uint64_t rows, uint64_t row_bytes, int world, int rank,
+                                      int64_t* ids, uint64_t cap);
+
 /* Write the CUDA IPC handle (UT_COOP_HANDLE_BYTES bytes) of this rank's region to handle_out and
  * its size to *region_bytes (may be NULL). Returns UT_OK, UT_EINVAL or UT_ECUDA. */
 UT_API int ut_coop_export(const ut_coop* c, void* handle_out, uint64_t* region_bytes);

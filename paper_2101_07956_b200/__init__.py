@@ -35,7 +35,8 @@ ABI = ("ut_register", "ut_gather", "ut_gather_host", "ut_release", "ut_error_pos
        "ut_graph_release", "ut_mem_advise", "ut_gather_dn", "ut_sample_async",
        "ut_sample_capacity", "ut_graph_launches", "ut_coop_create", "ut_coop_export",
        "ut_coop_open", "ut_coop_dispatch", "ut_coop_fetch", "ut_coop_combine", "ut_coop_gather",
-       "ut_coop_get_stats", "ut_coop_error_pos", "ut_coop_owner", "ut_coop_release")
+       "ut_coop_get_stats", "ut_coop_error_pos", "ut_coop_owner", "ut_coop_release",
+       "ut_coop_create_partitioned", "ut_coop_partition_ids")
 
 UT_COOP_HANDLE_BYTES = 64
 
@@ -119,6 +120,10 @@ def _load():
     L.ut_get_stats.argtypes = [vp, ctypes.POINTER(_Stats), ctypes.c_int]
     L.ut_coop_create.restype = vp
     L.ut_coop_create.argtypes = [vp, ctypes.c_int, ctypes.c_int, u64]
+    L.ut_coop_create_partitioned.restype = vp
+    L.ut_coop_create_partitioned.argtypes = [vp, u64, ctypes.c_int, ctypes.c_int, u64]
+    L.ut_coop_partition_ids.restype = ctypes.c_uint64
+    L.ut_coop_partition_ids.argtypes = [u64, u64, ctypes.c_int, ctypes.c_int, vp, u64]
     L.ut_coop_export.restype = ctypes.c_int
     L.ut_coop_export.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint64)]
     L.ut_coop_open.restype = ctypes.c_int
@@ -280,6 +285,24 @@ def ut_coop_create(t: int, world: int, rank: int, max_n: int) -> int:
         code, msg = last_error()
         raise UTError(code, msg)
     return h
+
+
+def ut_coop_create_partitioned(part: int, rows: int, world: int, rank: int, max_n: int) -> int:
+    h = _lib.ut_coop_create_partitioned(part, rows, world, rank, max_n)
+    if not h:
+        code, msg = last_error()
+        raise UTError(code, msg)
+    return h
+
+
+def ut_coop_partition_ids(rows: int, row_bytes: int, world: int, rank: int):
+    """int64 numpy array: the table row of each local row of `rank`'s partition (-1 = padding)."""
+    import numpy as np
+    k = int(_lib.ut_coop_partition_ids(rows, row_bytes, world, rank, None, 0))
+    ids = np.empty(k, dtype=np.int64)
+    if k:
+        _lib.ut_coop_partition_ids(rows, row_bytes, world, rank, ids.ctypes.data, k)
+    return ids
 
 
 def ut_coop_export(c: int) -> bytes:
@@ -469,7 +492,9 @@ class Coop:
     sync="host": dispatch / fetch / combine with a stream sync and a group barrier between."""
 
     def __init__(self, table: Table, max_n: int, group=None, rank: int | None = None,
-                 world: int | None = None, sync: str = "device"):
+                 world: int | None = None, sync: str = "device", rows: int | None = None):
+        """rows: None — `table` is the whole shared table; else the whole table's row count and
+        `table` is this rank's partition (rows ut.Coop.partition_ids(rows, rb, world, rank))."""
         import torch.distributed as dist
         if world is None:
             world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -478,18 +503,28 @@ class Coop:
         assert sync in ("device", "host")
         self.table, self.world, self.rank, self.sync, self.group = table, world, rank, sync, group
         self.max_n = int(max_n)
-        self.handle = ut_coop_create(table.handle, world, rank, self.max_n)
+        self.rows = int(rows) if rows is not None else table.rows
+        if rows is None:
+            self.handle = ut_coop_create(table.handle, world, rank, self.max_n)
+        else:
+            self.handle = ut_coop_create_partitioned(table.handle, self.rows, world, rank, self.max_n)
         if world > 1:
             # every rank must agree on the layout of the symmetric regions it is about to map
-            mine = (ut_coop_export(self.handle), (world, self.max_n, table.rows, table.row_bytes))
+            mine = (ut_coop_export(self.handle),
+                    (world, self.max_n, self.rows, table.row_bytes, rows is not None))
             allh = [None] * world
             dist.all_gather_object(allh, mine, group=group)
             shapes = {h[1] for h in allh}
             if len(shapes) != 1:
                 self.close()
-                raise UTError(UT_EINVAL, f"ranks disagree on (world, max_n, rows, row_bytes): {sorted(shapes)}")
+                raise UTError(UT_EINVAL, f"ranks disagree on (world, max_n, rows, row_bytes, partitioned): "
+                                         f"{sorted(shapes)}")
             ut_coop_open(self.handle, b"".join(h[0] for h in allh))
             dist.barrier(group=group)
+
+    @staticmethod
+    def partition_ids(rows: int, row_bytes: int, world: int, rank: int):
+        return ut_coop_partition_ids(rows, row_bytes, world, rank)
 
     def _barrier(self, stream) -> None:
         import torch

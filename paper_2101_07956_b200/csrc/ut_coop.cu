@@ -147,6 +147,7 @@ struct FetchArgs {
   uint32_t world;
   uint32_t epoch;
   Owner own;
+  bool partitioned;          // the fetch reads a per-rank partition at the row's local index
 };
 
 template <int PASS>
@@ -189,7 +190,7 @@ __global__ void k_dedup(FetchArgs f) {
       __syncthreads();
       if (win) {
         const uint64_t s = block_base + warp_tot[warp] + __popc(wm & ((1u << lane) - 1));
-        f.uniq[s] = id;
+        f.uniq[s] = f.partitioned ? (int64_t)l : id;
         f.wslot[e] = (uint32_t)s;
       }
       __syncthreads();                       // warp_tot / block_base reused next iteration
@@ -290,6 +291,7 @@ struct ut_coop {
   uint32_t* cnt = nullptr;
   unsigned long long* err = nullptr;
   uint32_t epoch = 0;                        // steps dispatched so far
+  bool partitioned = false;                  // t holds only this rank's rows, in local order
   uint64_t last_n = 0;
   uint64_t steps = 0, requested = 0, launches = 0, memops = 0;
   PWrite write32 = nullptr;
@@ -335,7 +337,8 @@ int check_dev(const ut_coop* c) {
 
 extern "C" {
 
-ut_coop* ut_coop_create(const ut_table* t, int world, int rank, uint64_t max_n) {
+static ut_coop* coop_create(const ut_table* t, uint64_t full_rows, bool partitioned, int world,
+                            int rank, uint64_t max_n) {
   if (!t) return set_err(UT_EINVAL, "table is NULL"), nullptr;
   if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
     return set_err(UT_EINVAL, "world %d / rank %d out of range (world <= %d)", world, rank, kMaxWorld), nullptr;
@@ -349,8 +352,13 @@ ut_coop* ut_coop_create(const ut_table* t, int world, int rank, uint64_t max_n) 
   c->world = world;
   c->rank = rank;
   c->cap = max_n;
-  c->rows = info.rows;
+  c->rows = partitioned ? full_rows : info.rows;
   c->rb = info.row_bytes;
+  c->partitioned = partitioned;
+  if (c->rows == 0) {
+    delete c;
+    return set_err(UT_EINVAL, "rows is 0"), nullptr;
+  }
   if (max_n > UINT64_MAX / 4 / c->rb / (uint64_t)world) {
     delete c;
     return set_err(UT_EINVAL, "world*max_n*row_bytes overflows"), nullptr;
@@ -361,6 +369,12 @@ ut_coop* ut_coop_create(const ut_table* t, int world, int rank, uint64_t max_n) 
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->dev);
   const uint64_t nblocks = (c->rows + c->own.R - 1) / c->own.R;
   c->tag_len = ((nblocks + world - 1) / world) * c->own.R;
+  if (partitioned && info.rows < c->tag_len) {
+    const uint64_t need = c->tag_len;
+    delete c;
+    return set_err(UT_EINVAL, "partition has %llu rows, this rank's blocks need %llu (ut_coop_partition_ids)",
+                   (unsigned long long)info.rows, (unsigned long long)need), nullptr;
+  }
   const uint64_t E = (uint64_t)world * max_n;
   cudaError_t e = cudaMalloc(&c->region, c->L.total);
   if (e == cudaSuccess) e = cudaMemset(c->region, 0, c->L.total);
@@ -388,6 +402,31 @@ ut_coop* ut_coop_create(const ut_table* t, int world, int rank, uint64_t max_n) 
     return nullptr;
   }
   return c;
+}
+
+ut_coop* ut_coop_create(const ut_table* t, int world, int rank, uint64_t max_n) {
+  return coop_create(t, 0, false, world, rank, max_n);
+}
+
+ut_coop* ut_coop_create_partitioned(const ut_table* part, uint64_t rows, int world, int rank,
+                                    uint64_t max_n) {
+  return coop_create(part, rows, true, world, rank, max_n);
+}
+
+uint64_t ut_coop_partition_ids(uint64_t rows, uint64_t row_bytes, int world, int rank, int64_t* ids,
+                               uint64_t cap) {
+  if (rows == 0 || row_bytes == 0 || world < 1 || rank < 0 || rank >= world) return 0;
+  const Owner o{block_rows(rows, row_bytes, world), (uint32_t)world};
+  const uint64_t nblocks = (rows + o.R - 1) / o.R;
+  const uint64_t local_rows = ((nblocks + world - 1) / world) * o.R;
+  if (ids && cap >= local_rows) {
+    for (uint64_t l = 0; l < local_rows; ++l) {
+      const uint64_t b = (l / o.R) * (uint64_t)world + (uint64_t)rank;   // inverse of Owner::local
+      const uint64_t id = b * o.R + l % o.R;
+      ids[l] = id < rows ? (int64_t)id : -1;
+    }
+  }
+  return local_rows;
 }
 
 int ut_coop_export(const ut_coop* c, void* handle_out, uint64_t* region_bytes) {
@@ -453,7 +492,7 @@ int ut_coop_fetch(ut_coop* c, ut_stream_t stream) {
   uint8_t* reg = c->region + parity_off(c);
   FetchArgs f{(const uint64_t*)(reg + c->L.count), (const int64_t*)(reg + c->L.inbox),
               (uint32_t*)(reg + c->L.slot), c->tag, c->wslot, c->uniq, c->u, c->cap,
-              (uint32_t)c->world, c->epoch, c->own};
+              (uint32_t)c->world, c->epoch, c->own, c->partitioned};
   const uint64_t E = c->cap * (uint64_t)c->world;
   cudaError_t e = cudaMemsetAsync(c->u, 0, 8, st);
   if (e != cudaSuccess) return cuda_err(e, "cudaMemsetAsync(unique count)");

@@ -123,15 +123,24 @@ def _worker(rank, world, port, cfg, q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         torch.cuda.set_device(0)
         rows, rb, n, steps, sync = cfg["rows"], cfg["rb"], cfg["n"], cfg["steps"], cfg["sync"]
-        hb = _table(rows, rb, seed=5)              # every rank its own copy of the same table
+        hb = _table(rows, rb, seed=5)              # every rank its own copy (the oracle's input)
         lists = _lists(rows, n, steps, rank, world, seed=rb + world)
+        part_kind = cfg.get("partition")            # the fetch then reads only this rank's rows
         if cfg.get("bad"):
             lists[-1] = lists[-1].copy()
             lists[-1][3] = rows + rank              # out of range at position 3
         if cfg.get("empty_rank") == rank:
             lists[1] = np.array([], dtype=np.int64)
         ok, fetched = True, []
-        with ut.Table(hb.addr, rows, rb) as t, ut.Coop(t, n, sync=sync) as c:
+        if part_kind:
+            ids = ut.Coop.partition_ids(rows, rb, world, rank)
+            t = ut.Table.create(ids.size, rb, part_kind)
+            workloads.fill_rows(t.host_addr, ids, rb, seed=5)
+            c = ut.Coop(t, n, sync=sync, rows=rows)
+        else:
+            t = ut.Table(hb.addr, rows, rb)
+            c = ut.Coop(t, n, sync=sync)
+        with t, c:
             prev = 0
             for k, l in enumerate(lists):
                 if cfg.get("overflow_rank") == rank and k == 1:
@@ -202,3 +211,26 @@ def test_processes_unaligned_rows_and_errors(rb):
 def test_processes_one_rank_bad_arguments_does_not_strand_peers():
     _run_world(3, {"rows": 20_000, "rb": 400, "n": 4000, "steps": 3, "sync": "device",
                    "overflow_rank": 1})
+
+
+@pytest.mark.parametrize("kind", ["managed", "pinned"])
+def test_partitioned_tables(kind):
+    """Each process holds only its own rows (ut_coop_create_partitioned), in the paper's managed
+    memory or pinned memory; outputs still equal the oracle's gather over the whole table."""
+    _run_world(2, {"rows": 40_000, "rb": 400, "n": 8000, "steps": 4, "sync": "device",
+                   "partition": kind, "bad": True})
+    _run_world(3, {"rows": 9000, "rb": 68, "n": 2000, "steps": 3, "sync": "host",
+                   "partition": kind})
+
+
+def test_world1_partitioned_is_the_table():
+    rows, rb = 5000, 100
+    hb = _table(rows, rb)
+    ids = ut.Coop.partition_ids(rows, rb, 1, 0)
+    assert (ids[ids >= 0] == np.arange(rows)).all()
+    with ut.Table.create(ids.size, rb, "pinned") as t:
+        workloads.fill_rows(t.host_addr, ids, rb, seed=11)
+        with ut.Coop(t, 3000, world=1, rank=0, rows=rows) as c:
+            for idx in _lists(rows, 3000, 2, 0, 1, seed=4):
+                _check_step(c, hb, rows, rb, idx)
+    hb.close()

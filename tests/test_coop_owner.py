@@ -61,3 +61,19 @@ def test_invalid_arguments():
 def test_create_rejects_null_table_without_cuda():
     with pytest.raises(ut.UTError):
         ut.ut_coop_create(0, 1, 0, 10)
+
+
+@pytest.mark.parametrize("rows,rb,world", [(1000, 68, 2), (5000, 4, 3), (777, 2408, 4), (3, 400, 5),
+                                           (10_000, 512, 1), (2_449_029, 400, 8)])
+def test_partition_ids_invert_ownership(rows, rb, world):
+    """The partitions of all ranks hold every row exactly once, and local row l of rank r's
+    partition is the row whose ut_coop_owner is (r, l) — the layout the partitioned fetch reads."""
+    seen = np.zeros(rows, dtype=np.int64)
+    for r in range(world):
+        ids = ut.ut_coop_partition_ids(rows, rb, world, r)
+        real = ids >= 0
+        seen[ids[real]] += 1
+        for l in np.flatnonzero(real)[:: max(1, real.sum() // 200)]:     # sampled on big tables
+            assert ut.ut_coop_owner(rows, rb, world, int(ids[l])) == (r, int(l))
+    assert (seen == 1).all()
+    assert ut.ut_coop_partition_ids(rows, rb, world, world).size == 0     # bad rank

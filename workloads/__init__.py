@@ -45,6 +45,9 @@ def lib():
         L.gen_fill_table.restype = None
         L.gen_fill_table.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
                                      ctypes.c_uint64, ctypes.c_int]
+        L.gen_fill_rows.restype = None
+        L.gen_fill_rows.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                    ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int]
         L.gen_uniform_idx.restype = None
         L.gen_uniform_idx.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
                                       ctypes.c_uint64]
@@ -86,6 +89,15 @@ def fill_table(dst, rows: int, rb: int, seed: int, threads: int = 0) -> None:
     if isinstance(dst, np.ndarray):
         assert dst.nbytes >= rows * rb
     lib().gen_fill_table(_addr(dst), rows, rb, seed & 0xFFFFFFFFFFFFFFFF, threads)
+
+
+def fill_rows(dst, ids: np.ndarray, rb: int, seed: int, threads: int = 0) -> None:
+    """Row k of ``dst`` = the content fill_table gives row ids[k] (zero row for ids[k] < 0)."""
+    ids = np.ascontiguousarray(ids, dtype=np.int64)
+    if isinstance(dst, np.ndarray):
+        assert dst.nbytes >= ids.size * rb
+    if ids.size:
+        lib().gen_fill_rows(_addr(dst), ids.ctypes.data, ids.size, rb, seed & 0xFFFFFFFFFFFFFFFF, threads)
 
 
 def uniform_idx(n: int, rows: int, seed: int) -> np.ndarray:

@@ -54,6 +54,33 @@ void gen_fill_table(uint8_t* dst, uint64_t rows, uint64_t rb, uint64_t seed, int
     }
 }
 
+/* Row k of dst = the self-identifying content of table row ids[k] (as gen_fill_table writes it);
+ * ids[k] < 0 gives a zero row. Fills a partition of a table, or the expected rows of a gather. */
+void gen_fill_rows(uint8_t* dst, const int64_t* ids, uint64_t n, uint64_t rb, uint64_t seed, int threads)
+{
+    int nt = threads > 0 ? threads : omp_get_max_threads();
+#pragma omp parallel for schedule(static, 4096) num_threads(nt)
+    for (int64_t k = 0; k < (int64_t)n; ++k) {
+        uint8_t* row = dst + (uint64_t)k * rb;
+        if (ids[k] < 0) {
+            memset(row, 0, rb);
+            continue;
+        }
+        uint64_t r = (uint64_t)ids[k];
+        uint64_t base = r * PHI;
+        uint64_t b = 0;
+        for (; b + 8 <= rb; b += 8) {
+            uint64_t w = splitmix64(seed ^ (base + b / 8));
+            memcpy(row + b, &w, 8);
+        }
+        if (b < rb) {
+            uint64_t w = splitmix64(seed ^ (base + b / 8));
+            memcpy(row + b, &w, rb - b);
+        }
+        memcpy(row, &r, rb < 8 ? rb : 8);
+    }
+}
+
 /* idx[i] = floor(splitmix64(seed ^ (i*PHI)) * rows / 2^64), i in [0, n). */
 void gen_uniform_idx(int64_t* idx, uint64_t n, uint64_t rows, uint64_t seed)
 {
