@@ -1,4 +1,3 @@
-R=gpurun_out/hugetlb; mkdir -p $R
+R=gpurun_out/cooprand; mkdir -p $R
 python -c "import __graft_entry__ as g; g.build()" > $R/build.log 2>&1
-cat /proc/meminfo | grep -i huge > $R/meminfo.txt; free -g >> $R/meminfo.txt
-timeout 900 python scripts/hugetlb_probe.py > $R/probe.jsonl 2> $R/probe.err
+timeout 900 python -m pytest tests/test_coop_gpu.py -q -x --timeout 300 -k "randomized or world1" > $R/pytest.log 2>&1; echo rc=$? >> $R/pytest.log

@@ -234,3 +234,26 @@ def test_world1_partitioned_is_the_table():
             for idx in _lists(rows, 3000, 2, 0, 1, seed=4):
                 _check_step(c, hb, rows, rb, idx)
     hb.close()
+
+
+def test_world1_randomized_instances():
+    """120 random (row width, base offset, rows, n, duplicates, bad ids, out offset) steps through
+    one cooperative handle per table, alternating buffer parities."""
+    import random
+    rng = random.Random(2101_07956)
+    for _ in range(12):
+        rb = rng.choice([1, 2, 3, 4, 8, 12, 16, 36, 68, 100, 128, 400, 512, 1372, 2052, 2408, 4096])
+        rows = rng.randint(1, 4000)
+        off = rng.randint(0, 15)
+        hb = _table(rows, rb, seed=rb + rows, offset=off)
+        with ut.Table(hb.addr, rows, rb) as t, ut.Coop(t, 3000, world=1, rank=0,
+                                                        sync=rng.choice(["device", "host"])) as c:
+            for _ in range(10):
+                n = rng.choice([0, 1, 2, rng.randint(1, 3000)])
+                idx = np.array([rng.randrange(rows) for _ in range(n)], dtype=np.int64)
+                if n and rng.random() < 0.3:
+                    idx[rng.randrange(n)] = rng.choice([-1, rows, rows + 7, -2**40])
+                if n > 3 and rng.random() < 0.3:
+                    idx[: n // 2] = idx[0]                      # heavy duplication
+                _check_step(c, hb, rows, rb, idx, offset=rng.randint(0, 15))
+        hb.close()
