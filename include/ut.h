@@ -186,7 +186,9 @@ UT_API const char* ut_plan_probe(uint64_t base, uint64_t rows, uint64_t row_byte
 
 /*
  * ut_set_plan — force a kernel variant by kind for A/B measurement: "narrow", "vec16",
- * "vec16x", "realign", "realignx", or "auto" (the default choice). A kind whose preconditions
+ * "vec16x", "realign", "realignx", the TMA variants "bulk" (1-D bulk copy per row) and "tma4"
+ * (tensor-map tile::gather4, 4 rows per instruction), the paper's "paper_naive" / "paper_shift",
+ * or "auto" (the default choice). A kind whose preconditions
  * the table violates returns UT_EINVAL and leaves the plan unchanged; every admissible kind is
  * correct for any output alignment (ut_gather falls back to "auto" for an output it cannot take).
  * "timing=on|off" brackets each gather-kernel launch with CUDA events (see ut_get_stats).

@@ -131,7 +131,7 @@ constexpr int kMaxDev = 64;
 
 // ---- plans ------------------------------------------------------------------------------------
 enum PlanKind { P_AUTO = -1, P_NARROW = 0, P_VEC16 = 1, P_VEC16X = 2, P_REALIGN = 3, P_REALIGNX = 4, P_BULK = 5,
-                P_PAPER_NAIVE = 6, P_PAPER_SHIFT = 7 };
+                P_PAPER_NAIVE = 6, P_PAPER_SHIFT = 7, P_TMA4 = 8 };
 
 struct Plan {
   PlanKind kind;
@@ -153,6 +153,7 @@ const char* plan_name(const Plan& p) {
                      case 8: return "realign.g8"; case 16: return "realign.g16"; default: return "realign.g32"; }
     case P_REALIGNX: return "realign.g32x";
     case P_BULK: return "bulk";
+    case P_TMA4: return "tma4";
     case P_PAPER_NAIVE: return "paper_naive";
     case P_PAPER_SHIFT: return "paper_shift";
     default: return "invalid";
@@ -208,6 +209,10 @@ bool choose_plan(uint64_t base, uint64_t rows, uint64_t rb, uint64_t out, PlanKi
     case P_REALIGNX:
       *p = Plan{k, 32, clip};
       return true;
+    case P_TMA4:
+      if (!aligned || rb > (uint64_t)ut::kTma4MaxRow || rows >= (1ull << 31)) return false;
+      *p = Plan{k, 32, false};
+      return true;
     case P_BULK:
       if (!aligned || rb > (uint64_t)ut::kBulkMaxRow) return false;
       *p = Plan{k, 32, false};
@@ -231,6 +236,7 @@ PlanKind parse_plan(const char* s, bool* ok) {
   if (!strcmp(s, "realign")) return P_REALIGN;
   if (!strcmp(s, "realignx")) return P_REALIGNX;
   if (!strcmp(s, "bulk")) return P_BULK;
+  if (!strcmp(s, "tma4")) return P_TMA4;
   if (!strcmp(s, "paper_naive")) return P_PAPER_NAIVE;
   if (!strcmp(s, "paper_shift")) return P_PAPER_SHIFT;
   *ok = false;
@@ -259,6 +265,8 @@ struct DevState {
   cudaEvent_t drained[kBuf] = {};
   int64_t* idx_all = nullptr;           // ut_gather_host zero-copy path: device copy of idx
   uint64_t idx_cap = 0;
+  CUtensorMap tmap;                     // "tma4" plan: the table as a rows x (rb/4) word tensor
+  bool tmap_ok = false;
 };
 
 }  // namespace
@@ -473,6 +481,20 @@ cudaError_t launch_plan(const Plan& p, int sms, cudaStream_t st, const ut::Gathe
       else ut::k_paper<true><<<grid, 256, 0, st>>>(a);
       return cudaGetLastError();
     }
+    case P_TMA4: {
+      if (PERM || !a.tmap) return cudaErrorInvalidValue;    // A/B plan: index order only
+      constexpr int U = 4;
+      const int slot = (int)((4 * a.rb + 127) & ~127ull);
+      const int smem = 4 * U * slot;
+      cudaFuncSetAttribute(ut::k_tma4<U>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ut::k_tma4<U>, 128, smem);
+      if (per_sm <= 0) per_sm = 1;
+      const uint64_t tiles = ((a.n + 3) / 4 + U - 1) / U;
+      const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)sms * per_sm, (tiles + 3) / 4));
+      ut::k_tma4<U><<<grid, 128, smem, st>>>(*a.tmap, a);
+      return cudaGetLastError();
+    }
     case P_BULK: {
       constexpr int U = 4;
       auto k = ut::k_bulk<U, PERM>;
@@ -555,6 +577,33 @@ cudaError_t launch_staged(const ut_table* t, DevState* s, cudaStream_t st, const
 
 int gather_runs(const ut_table* t, DevState* s, const Plan& p, const ut::GatherArgs& a, cudaStream_t st);
 
+// The table as a 2-D tensor of rows x (rb/4) 32-bit words for the "tma4" plan (built once per
+// device; cuTensorMapEncodeTiled through the runtime's driver entry point).
+int tensor_map(const ut_table* ct, DevState* s) {
+  ut_table* t = const_cast<ut_table*>(ct);
+  std::lock_guard<std::mutex> lk(t->mu);
+  if (s->tmap_ok) return UT_OK;
+  typedef CUresult (*PEncode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return set_err(UT_ENOTSUP, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {t->rb / 4, t->rows};
+  const cuuint64_t strides[1] = {t->rb};
+  const cuuint32_t box[2] = {(cuuint32_t)(t->rb / 4), 1};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = reinterpret_cast<PEncode>(fn)(&s->tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, (void*)s->dev_base,
+                                             dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(UT_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  s->tmap_ok = true;
+  return UT_OK;
+}
+
 int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n, void* out_dev,
               cudaStream_t st, bool host_out = false, const uint64_t* n_dev = nullptr) {
   Plan p;
@@ -562,11 +611,17 @@ int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n
       !choose_plan((uint64_t)t->host, t->rows, t->rb, (uint64_t)out_dev, P_AUTO, &p))
     return set_err(UT_EINVAL, "no admissible plan");
   ut::GatherArgs a{s->dev_base, t->rows, t->rb, idx_dev, n, (uint64_t)out_dev, s->err, nullptr, n_dev};
+  if (p.kind == P_TMA4) {
+    int rc = tensor_map(t, s);
+    if (rc != UT_OK) return rc;
+    a.tmap = &s->tmap;
+  }
   cudaError_t e;
   s->rows += n;
   s->bytes += n * t->rb;
   const bool runs = want_runs(t, p, n);
-  if (!runs && (!want_reorder(t, n) || p.kind == P_PAPER_NAIVE || p.kind == P_PAPER_SHIFT)) {
+  if (!runs && (!want_reorder(t, n) || p.kind == P_PAPER_NAIVE || p.kind == P_PAPER_SHIFT ||
+                p.kind == P_TMA4)) {
     if (host_out && want_stage(t, (uint64_t)out_dev, p)) {
       e = timed(t, s, st, [&] { return launch_staged(t, s, st, a); });
       if (e != cudaSuccess) return cuda_err(e, "staged gather");

@@ -25,6 +25,8 @@
 // end is not 16-B aligned). An index < 0 or >= rows zero-fills its row and atomicMin's its
 // position into *err (reading R4).
 #pragma once
+#include <cuda.h>
+
 #include <cstdint>
 
 #ifndef UT_MINB
@@ -162,6 +164,7 @@ struct GatherArgs {
   unsigned long long* err;
   const uint32_t* perm;   // optional visiting order (work item j handles output row perm[j])
   const uint64_t* n_dev;  // optional: the row count lives in device memory (min(*n_dev, n))
+  const CUtensorMap* tmap = nullptr;   // host copy of the table's tensor map ("tma4" plan only)
 };
 
 // The kernels' view of the arguments: n read from device memory when the launch is
@@ -532,6 +535,83 @@ __global__ void __launch_bounds__(256, 1) k_bulk(GatherArgs a_) {
         while (!mbar_try_wait(bar0 + 8u * u, phase)) {
         }
       }
+    }
+    phase ^= 1u;
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// tma4<U>: the TMA unit's row gather (cp.async.bulk.tensor.2d ... tile::gather4): one instruction
+// fetches 4 rows of the table, viewed as a 2-D tensor of rows x (rb/4) 32-bit words, into shared
+// memory; the warp then stores them to HBM. A/B plan only (SURVEY §7 step 4 "TMA tile::gather4 for
+// rb % 16 == 0 tables"). rb % 16 == 0, rb <= 1024 (box width <= 256 words), rows < 2^31. Rows
+// past n, and bad indices (mapped to the out-of-bounds coordinate `rows`), are zero-filled by the
+// TMA unit without touching memory. One warp per group of 4 rows, U groups in flight per warp.
+constexpr int kTma4MaxRow = 1024;
+
+template <int U>
+__global__ void __launch_bounds__(128, 1) k_tma4(const __grid_constant__ CUtensorMap tm, GatherArgs a_) {
+  const GatherArgs a = with_dev_n(a_);
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bars[4 * U];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const uint32_t slot = (uint32_t)((4 * a.rb + 127) & ~127ull);
+  uint8_t* my = smem + (size_t)wib * U * slot;
+  const uint32_t bar0 = smem_u32(&bars[wib * U]);
+  if (lane == 0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8u * u) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t ngroups = (a.n + 3) / 4;
+  const uint64_t ntiles = (ngroups + U - 1) / U;
+  uint32_t phase = 0;
+  for (uint64_t tile = warp; tile < ntiles; tile += nwarps) {
+    if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t g = tile * U + u;
+      // lanes 0..3 read the group's 4 indices; lane 0 issues the gather (always, so every
+      // barrier completes one phase per tile; rows past n use the out-of-bounds coordinate)
+      int32_t crd = (int32_t)a.rows;
+      if (lane < 4) {
+        const uint64_t i = g * 4 + lane;
+        if (i < a.n) {
+          const int64_t r = __ldg(a.idx + i);
+          if ((uint64_t)r < a.rows) crd = (int32_t)r;
+          else record_bad(a.err, i);
+        }
+      }
+      const int32_t c0 = __shfl_sync(0xffffffffu, crd, 0), c1 = __shfl_sync(0xffffffffu, crd, 1);
+      const int32_t c2 = __shfl_sync(0xffffffffu, crd, 2), c3 = __shfl_sync(0xffffffffu, crd, 3);
+      if (lane == 0) {
+        const uint32_t bar = bar0 + 8u * u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"((uint32_t)(4 * a.rb))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(my + (size_t)u * slot)),
+            "l"(&tm), "r"(0), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+            : "memory");
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t g = tile * U + u;
+      while (!mbar_try_wait(bar0 + 8u * u, phase)) {
+      }
+      const uint64_t i0 = g * 4;
+      const uint64_t nr = i0 < a.n ? (a.n - i0 < 4 ? a.n - i0 : 4) : 0;
+      const uint32_t bytes = (uint32_t)(nr * a.rb);
+      for (uint32_t c = lane * 16; c < bytes; c += 32 * 16)
+        st16(a.out + i0 * a.rb + c, *reinterpret_cast<const V4*>(my + (size_t)u * slot + c));
     }
     phase ^= 1u;
     __syncwarp();

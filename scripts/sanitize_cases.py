@@ -21,7 +21,7 @@ for rb, off in [(4, 0), (8, 8), (68, 3), (400, 0), (400, 4), (2052, 1), (4096, 0
     idx[:2] = [0, rows - 1]
     want, _ = oracle.gather(hb.addr, rows, rb, idx)
     with ut.Table(hb.addr, rows, rb) as t:
-        for plan in ["auto", "realign", "realignx", "vec16", "vec16x", "narrow", "bulk",
+        for plan in ["auto", "realign", "realignx", "vec16", "vec16x", "narrow", "bulk", "tma4",
                      "paper_naive", "paper_shift"]:
             try:
                 t.set_plan(plan)

@@ -69,7 +69,7 @@ def test_randomized_instances(pinned_pool):
     widths = [1, 2, 3, 4, 5, 7, 8, 12, 16, 17, 24, 31, 32, 33, 48, 64, 68, 100, 127, 128, 129,
               132, 256, 260, 400, 500, 511, 512, 513, 516, 1024, 1028, 1172, 1372, 2048, 2052,
               2056, 2064, 2076, 2408, 3200, 4092, 4095, 4096, 5000, 8192, 16384]
-    plans = [None, "realign", "realignx", "vec16", "vec16x", "narrow", "bulk", "paper_naive", "paper_shift"]
+    plans = [None, "realign", "realignx", "vec16", "vec16x", "narrow", "bulk", "tma4", "paper_naive", "paper_shift"]
     done = 0
     for it in range(1100):
         rb = rng.choice(widths) if it % 3 else rng.randint(1, 6000)
@@ -120,7 +120,7 @@ def test_guard_page_no_over_read(rb, pad):
     idx = np.array([rows - 1, 0, rows - 1, rows // 2, 0, rows - 1] * 7, dtype=np.int64)
     with ut.Table(hb.addr, rows, rb) as t:
         assert t.info()["registered"] == 1
-        for plan in [None, "realign", "realignx", "vec16", "vec16x", "narrow", "bulk", "paper_naive", "paper_shift"]:
+        for plan in [None, "realign", "realignx", "vec16", "vec16x", "narrow", "bulk", "tma4", "paper_naive", "paper_shift"]:
             try:
                 if plan:
                     t.set_plan(plan)
