@@ -254,7 +254,7 @@ def sm_read_ceiling(torch, ut, nbytes: int = 1 << 30, reps: int = 5) -> float:
 NCU_TRAFFIC = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
 
 
-def ncu_traffic(workload: str, plan: str, args) -> dict:
+def ncu_traffic(workload: str, plan: str, table_memory: str, args) -> dict:
     """roofline.traffic from the committed ncu capture of this workload's timed gathers
     (profiles/ncu_traffic.json, written by scripts/ncu_summary.py --traffic): HBM bytes
     (dram__bytes_read.sum + dram__bytes_write.sum) per gather launch, averaged over the captured
@@ -265,7 +265,8 @@ def ncu_traffic(workload: str, plan: str, args) -> dict:
             rec = json.load(f).get(workload)
     except (OSError, ValueError):
         rec = None
-    if not rec or rec.get("plan") != plan or args.plan or args.sample != "cpu" or args.coop != "off":
+    if (not rec or rec.get("plan") != plan or rec.get("table_memory", table_memory) != table_memory
+            or args.plan or args.sample != "cpu" or args.coop != "off"):
         return {"traffic": None}
     return {"traffic": rec["hbm_bytes_per_launch"],
             "traffic_detail": {k: rec[k] for k in ("hbm_bytes_per_launch", "hbm_write_bytes_per_launch",
@@ -673,7 +674,7 @@ def run_ut(args, spec, dist):
                          "achieved": round(achieved, 3) if achieved is not None else None,
                          "peak": round(link, 3), "unit": "GB/s",
                          "frac": round(achieved / link, 4) if achieved is not None else None,
-                         **ncu_traffic(spec["workload"], table.plan, args),
+                         **ncu_traffic(spec["workload"], table.plan, args.alloc, args),
                          "kernel": f"gather {table.plan} (device time of the gather kernel alone, CUDA events on its stream)",
                          "peak_source": "pinned cudaMemcpy H2D measured in this run (best of 10 x 1 GiB)",
                          "sm_read_ceiling": round(sm_ceiling, 3)},

@@ -64,7 +64,8 @@ def traffic(csv_path, bench_path, out_path):
     line = json.loads([x for x in open(bench_path).read().splitlines() if x.startswith("{")][-1])
     cfg = line["config"]
     rec = {
-        "plan": line["plan"], "launches": n, "kernel": launches[0]["kernel"] if n else None,
+        "plan": line["plan"], "table_memory": line.get("table_memory"), "launches": n,
+        "kernel": launches[0]["kernel"] if n else None,
         "hbm_bytes_per_launch": round(avg("dram__bytes_read.sum") + avg("dram__bytes_write.sum")),
         "hbm_read_bytes_per_launch": round(avg("dram__bytes_read.sum")),
         "hbm_write_bytes_per_launch": round(avg("dram__bytes_write.sum")),
