@@ -543,6 +543,9 @@ def run_ut(args, spec, dist):
     dev_ms = evs[0] if (sampler is not None and args.pipeline) else sum(a.elapsed_time(b) for a, b in evs)
 
     own_launches = st["kernel_launches"]
+    # the gather variant of the timed steps: the table's plan, "+share" when the gathers took
+    # neighbour line sharing
+    plan_label = table.plan + ("+share" if st.get("share_gathers") else "")
     coop_block = None
     if coop is not None:
         c1 = coop.stats()
@@ -666,7 +669,7 @@ def run_ut(args, spec, dist):
             "frac_of_link": round(per_gpu / link, 4),
             "sm_read_ceiling_gbs": round(sm_ceiling, 3),
             "frac_of_sm_read_ceiling": round(per_gpu / sm_ceiling, 4),
-            "plan": table.plan,
+            "plan": plan_label,
             "table_memory": args.alloc + (" (per-rank partitions, ut_coop_create_partitioned)" if partitioned else ""),
             "numa": {"nodes": workloads.numa_nodes(), "gpu_node": gnode,
                      "table_policy": "interleave" if getattr(hb, "numa", 0) > 1 else "single node / default"},
@@ -674,8 +677,8 @@ def run_ut(args, spec, dist):
                          "achieved": round(achieved, 3) if achieved is not None else None,
                          "peak": round(link, 3), "unit": "GB/s",
                          "frac": round(achieved / link, 4) if achieved is not None else None,
-                         **ncu_traffic(spec["workload"], table.plan, args.alloc, args),
-                         "kernel": f"gather {table.plan} (device time of the gather kernel alone, CUDA events on its stream)",
+                         **ncu_traffic(spec["workload"], plan_label, args.alloc, args),
+                         "kernel": f"gather {plan_label} (device time of the gather kernel alone, CUDA events on its stream)",
                          "peak_source": "pinned cudaMemcpy H2D measured in this run (best of 10 x 1 GiB)",
                          "sm_read_ceiling": round(sm_ceiling, 3)},
             "cpu_baseline": cpu_base, "py_baseline": py_base, "e2e": e2e,

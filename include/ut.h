@@ -194,6 +194,10 @@ UT_API const char* ut_plan_probe(uint64_t base, uint64_t rows, uint64_t row_byte
  * "timing=on|off" brackets each gather-kernel launch with CUDA events (see ut_get_stats).
  * "runs=on|off" (default off): for 16-B aligned tables, sort the rows exactly and copy runs of
  * table-adjacent rows with one warp so shared boundary lines are requested once.
+ * "share=on|off|auto": neighbour line sharing for 16-B aligned tables with 128 < rb <= 512 —
+ * the warp of a selected row also fetches its selected successor's bytes in the 128-B line the
+ * two share, so the line is requested once; auto = on for gathers of >= 64K rows
+ * that select >= 1/16 of the table. Costs rows x 4 B of stream-ordered scratch per gather.
  * "stage=on|off|auto" (auto = off): ut_gather_host's direct path gathers tiles of consecutive
  * output rows into shared memory and writes each tile's span with whole-line stores (k_staged;
  * an A/B knob — measured no gain).
@@ -294,6 +298,7 @@ typedef struct ut_stats {
   uint64_t bytes;            /* rows * row_bytes                                                     */
   uint64_t timed_launches;   /* gather-kernel launches bracketed by events ("timing=on")            */
   double gather_kernel_ms;   /* their summed device time (CUDA events on the launch stream)          */
+  uint64_t share_gathers;    /* gathers that took neighbour line sharing ("share")    */
 } ut_stats;
 
 /*

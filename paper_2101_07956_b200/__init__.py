@@ -60,7 +60,8 @@ class _Info(ctypes.Structure):
 class _Stats(ctypes.Structure):
     _fields_ = [("gathers", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
                 ("rows", ctypes.c_uint64), ("bytes", ctypes.c_uint64),
-                ("timed_launches", ctypes.c_uint64), ("gather_kernel_ms", ctypes.c_double)]
+                ("timed_launches", ctypes.c_uint64), ("gather_kernel_ms", ctypes.c_double),
+                ("share_gathers", ctypes.c_uint64)]
 
 
 class _CoopStats(ctypes.Structure):

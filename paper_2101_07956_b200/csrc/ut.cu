@@ -250,7 +250,7 @@ struct DevState {
   int sms = 0;
   cudaMemPool_t pool = nullptr;         // stream-ordered scratch for the reorder stage
   // counters (ut_get_stats)
-  std::atomic<uint64_t> gathers{0}, launches{0}, rows{0}, bytes{0};
+  std::atomic<uint64_t> gathers{0}, launches{0}, rows{0}, bytes{0}, shared{0};
   std::mutex tmu;                       // timing events
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending, spare;
   uint64_t timed = 0;
@@ -287,6 +287,7 @@ struct ut_table {
   int conc = -1;                        // launch shape: -1 auto, 0 dense, 1 sparse ("conc=...")
   int runs = -1;                        // run merge: -1 auto, 0 off, 1 on ("runs=...")
   int stage = -1;                       // host-output tile staging: -1 auto (= off), 0 off, 1 on ("stage=...")
+  int share = -1;                       // neighbour line sharing: -1 auto, 0 off, 1 on ("share=...")
   std::mutex mu;
   DevState dev[kMaxDev];
 };
@@ -576,6 +577,8 @@ cudaError_t launch_staged(const ut_table* t, DevState* s, cudaStream_t st, const
 }
 
 int gather_runs(const ut_table* t, DevState* s, const Plan& p, const ut::GatherArgs& a, cudaStream_t st);
+bool want_share(const ut_table* t, const Plan& p, uint64_t n);
+int gather_share(const ut_table* t, DevState* s, const ut::GatherArgs& a, cudaStream_t st);
 
 // The table as a 2-D tensor of rows x (rb/4) 32-bit words for the "tma4" plan (built once per
 // device; cuTensorMapEncodeTiled through the runtime's driver entry point).
@@ -619,6 +622,7 @@ int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n
   cudaError_t e;
   s->rows += n;
   s->bytes += n * t->rb;
+  if (want_share(t, p, n)) return gather_share(t, s, a, st);
   const bool runs = want_runs(t, p, n);
   if (!runs && (!want_reorder(t, n) || p.kind == P_PAPER_NAIVE || p.kind == P_PAPER_SHIFT ||
                 p.kind == P_TMA4)) {
@@ -793,6 +797,51 @@ int gather_runs(const ut_table* t, DevState* s, const Plan& p, const ut::GatherA
   cudaError_t e2 = cudaFreeAsync(scratch, st);
   if (e != cudaSuccess) return cuda_err(e, "run-merge gather");
   if (e2 != cudaSuccess) return cuda_err(e2, "cudaFreeAsync(run scratch)");
+  return UT_OK;
+}
+
+// Neighbour line sharing: vec16 tables with 128 < rb <= 512 whose row boundaries
+// are not all on 128-B lines. "auto" takes it for gathers of >= 64K rows that select >= 1/16 of
+// the table (so that a selected row's successor is selected often enough to pay for the
+// rows x 4 B slot array), with the slot array <= 1 GiB.
+bool want_share(const ut_table* t, const Plan& p, uint64_t n) {
+  if (t->share == 0 || p.kind != P_VEC16 || t->rb <= 128 || t->rb > 512) return false;
+  if ((((uint64_t)t->host | t->rb) & 127) == 0) return false;     // no partial lines to share
+  if (n == 0 || n >= (1ull << 31) || t->rows > (1ull << 28)) return false;
+  if (t->share == 1) return true;
+  if (t->reorder == 1 || t->runs == 1) return false;
+  return n >= 65536 && n * 16 >= t->rows;
+}
+
+int gather_share(const ut_table* t, DevState* s, const ut::GatherArgs& a, cudaStream_t st) {
+  uint32_t* slot = nullptr;
+  cudaError_t e;
+  if ((e = cudaMallocFromPoolAsync((void**)&slot, t->rows * sizeof(uint32_t), s->pool, st)) != cudaSuccess)
+    return cuda_err(e, "cudaMallocFromPoolAsync(share slots)");
+  e = cudaMemsetAsync(slot, 0, t->rows * sizeof(uint32_t), st);
+  if (e == cudaSuccess) {
+    const int gm = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)s->sms * 8, (a.n + 255) / 256));
+    ut::k_share_mark<<<gm, 256, 0, st>>>(a, slot);
+    s->launches += 1;
+    s->shared += 1;
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) {
+    e = timed(t, s, st, [&] {
+      const uint64_t tiles = (a.n + kU - 1) / kU;
+      if (t->rb > 400) {
+        auto k = ut::k_share<kU, true>;
+        k<<<grid_for(k, s->sms, tiles, -2), 256, 0, st>>>(a, slot);
+      } else {
+        auto k = ut::k_share<kU, false>;
+        k<<<grid_for(k, s->sms, tiles, -2), 256, 0, st>>>(a, slot);
+      }
+      return cudaGetLastError();
+    });
+  }
+  cudaError_t e2 = cudaFreeAsync(slot, st);
+  if (e != cudaSuccess) return cuda_err(e, "shared-line gather");
+  if (e2 != cudaSuccess) return cuda_err(e2, "cudaFreeAsync(share slots)");
   return UT_OK;
 }
 
@@ -1261,6 +1310,14 @@ int ut_set_plan(ut_table* t, const char* name) {
     else return set_err(UT_EINVAL, "runs must be auto|on|off, got '%s'", v);
     return UT_OK;
   }
+  if (!strncmp(name, "share=", 6)) {
+    const char* v = name + 6;
+    if (!strcmp(v, "auto")) t->share = -1;
+    else if (!strcmp(v, "on")) t->share = 1;
+    else if (!strcmp(v, "off")) t->share = 0;
+    else return set_err(UT_EINVAL, "share must be auto|on|off, got '%s'", v);
+    return UT_OK;
+  }
   if (!strncmp(name, "stage=", 6)) {
     const char* v = name + 6;
     if (!strcmp(v, "auto")) t->stage = -1;
@@ -1317,7 +1374,9 @@ int ut_get_stats(const ut_table* t, ut_stats* st, int reset) {
   st->bytes = s->bytes;
   st->timed_launches = s->timed;
   st->gather_kernel_ms = s->timed_ms;
+  st->share_gathers = s->shared;
   if (reset) {
+    s->shared = 0;
     s->gathers = 0;
     s->launches = 0;
     s->rows = 0;

@@ -830,4 +830,84 @@ __global__ void __launch_bounds__(256) k_runs(GatherArgs a_, const uint32_t* __r
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Neighbour line sharing ("share", vec16 tables with 128 < rb <= 512). Selected
+// rows r and r+1 whose boundary does not fall on a 128-B line both touch that line; fetched by
+// both warps it costs two sysmem requests, and at these widths the request count, not the bytes,
+// bounds the link. k_share_mark gives every selected row one canonical work item,
+// slot[r] = i + 1 (0 = not selected; any one occurrence of a duplicated row wins). In k_share
+// the warp of row r also loads the bytes of row r+1 that lie in r's last line and stores them
+// into row r+1's canonical output row; that canonical item skips its first (shared) line. Both
+// sides decide from the same slot[] — fixed for the whole gather — so every output byte is
+// written by its own row's warp or by a predecessor's warp that read the same table bytes
+// (duplicates of r write identical bytes). The result is the plain gather (oracle), unchanged.
+__global__ void __launch_bounds__(256) k_share_mark(GatherArgs a_, uint32_t* __restrict__ slot) {
+  const GatherArgs a = with_dev_n(a_);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+    const int64_t r = __ldg(a.idx + i);
+    if ((uint64_t)r < a.rows) slot[r] = (uint32_t)(i + 1);
+  }
+}
+
+// One warp per row step, U steps in flight per warp; lane q moves 16-B chunk q (and q + 32 when
+// TWO, rows > 400 B) of the byte range [lo, hi) relative to the row start: lo skips the shared
+// first line, hi extends over the successor's bytes in the last line.
+template <int U, bool TWO>
+__global__ void __launch_bounds__(256, UT_MINB) k_share(GatherArgs a_, const uint32_t* __restrict__ slot) {
+  const GatherArgs a = with_dev_n(a_);
+  constexpr int C = TWO ? 2 : 1;
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t ntiles = (a.n + U - 1) / U;
+  for (uint64_t tile = warp; tile < ntiles; tile += nwarps) {
+    V4 cur[U][C];
+    uint64_t ii[U], nxt[U];
+    uint32_t lo[U], hi[U];
+    bool inb[U], ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = ii[u] = tile * U + u;
+      inb[u] = i < a.n;
+      const int64_t r = inb[u] ? __ldg(a.idx + i) : 0;
+      ok[u] = inb[u] && (uint64_t)r < a.rows;
+      const uint64_t s = a.tbase + (ok[u] ? (uint64_t)r : 0ull) * a.rb;
+      lo[u] = 0;
+      hi[u] = (uint32_t)a.rb;
+      nxt[u] = 0;
+      if (ok[u]) {
+        if ((s & 127) && r > 0 && __ldg(slot + r) == (uint32_t)(i + 1) && __ldg(slot + r - 1) != 0u)
+          lo[u] = 128u - (uint32_t)(s & 127);
+        const uint64_t e = s + a.rb;
+        if ((e & 127) && (uint64_t)r + 1 < a.rows) {
+          const uint32_t nx = __ldg(slot + r + 1);
+          if (nx) {
+            hi[u] = (uint32_t)a.rb + 128u - (uint32_t)(e & 127);
+            nxt[u] = nx;
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const uint32_t b = 16u * (uint32_t)(lane + 32 * c);
+        cur[u][c] = (ok[u] && b >= lo[u] && b < hi[u]) ? ld_table16(s + b) : v4_zero();
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!inb[u]) continue;
+      const uint64_t d = a.out + ii[u] * a.rb;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const uint32_t b = 16u * (uint32_t)(lane + 32 * c);
+        if (b < lo[u] || b >= hi[u]) continue;
+        if (b < a.rb) st16(d + b, cur[u][c]);
+        else st16(a.out + (nxt[u] - 1) * a.rb + (b - a.rb), cur[u][c]);
+      }
+      if (!ok[u] && lane == 0) record_bad(a.err, ii[u]);
+    }
+  }
+}
+
 }  // namespace ut

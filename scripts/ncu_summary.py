@@ -50,7 +50,7 @@ def traffic(csv_path, bench_path, out_path):
     per = defaultdict(dict)
     for r in rows[1:]:
         name = r[h.index("Kernel Name")]
-        if not re.search(r"\bk_(single|multi|narrow|runs|paper|bulk)\b", name):
+        if not re.search(r"\bk_(single|multi|narrow|runs|paper|bulk|share)\b", name):
             continue
         unit = r[h.index("Metric Unit")]
         v = float(r[h.index("Metric Value")].replace(",", ""))

@@ -1,5 +1,5 @@
 """Tiny cases for compute-sanitizer (memcheck / racecheck / synccheck): every kernel family,
-the reorder stage, the TMA bulk plan, the paper's kernels, host end-to-end, GPU sampling and
+the reorder stage, run merge, neighbour line sharing, the TMA bulk plan, the paper's kernels, host end-to-end, GPU sampling and
 the cooperative gather (one rank: dispatch, dedup, host fetch, combine)."""
 import os
 import sys
@@ -13,7 +13,7 @@ import paper_2101_07956_b200 as ut
 import workloads
 
 bad = 0
-for rb, off in [(4, 0), (8, 8), (68, 3), (400, 0), (400, 4), (2052, 1), (4096, 0), (13, 5)]:
+for rb, off in [(4, 0), (8, 8), (68, 3), (400, 0), (400, 4), (144, 0), (2052, 1), (4096, 0), (13, 5)]:
     rows = 3000
     hb = workloads.HostBuffer(rows * rb, kind="guarded")
     workloads.fill_table(hb.addr, rows, rb, rb)
@@ -27,16 +27,18 @@ for rb, off in [(4, 0), (8, 8), (68, 3), (400, 0), (400, 4), (2052, 1), (4096, 0
                 t.set_plan(plan)
             except ut.UTError:
                 continue
-            for reorder in ["reorder=off", "reorder=on", "runs=on"]:
-                t.set_plan(reorder)
+            for reorder in ["reorder=off,runs=off,share=off", "reorder=on,runs=off,share=off",
+                            "reorder=off,runs=on,share=off", "reorder=off,runs=off,share=on"]:
+                for m in reorder.split(","):
+                    t.set_plan(m)
                 buf = torch.zeros(700 * rb + 16, dtype=torch.uint8, device="cuda")
                 t.gather(torch.from_numpy(idx).cuda(), out=buf[off: off + 700 * rb])
                 got = buf[off: off + 700 * rb].cpu().numpy()
                 if got.tobytes() != want.tobytes():
                     bad += 1
                     print("MISMATCH", rb, plan, reorder)
-        t.set_plan("auto")
-        t.set_plan("reorder=auto")
+        for m in ["auto", "reorder=auto", "runs=auto", "share=auto"]:
+            t.set_plan(m)
         o = t.gather_host(torch.from_numpy(idx).pin_memory())
         bad += o.numpy().tobytes() != want.tobytes()
     hb.close()

@@ -93,6 +93,7 @@ def test_randomized_instances(pinned_pool):
                 t.set_plan("reorder=on")                # translation-locality visiting order
             t.set_plan("conc=" + rng.choice(["auto", "dense", "sparse"]))   # launch shape
             t.set_plan("runs=" + rng.choice(["auto", "on", "off"]))          # run merge
+            t.set_plan("share=" + rng.choice(["auto", "on", "off"]))         # line sharing
             plan = rng.choice(plans)
             if plan is not None:
                 try:
@@ -276,6 +277,62 @@ def test_run_merge_dense_and_adjacent(rb, off):
             t.set_plan(mode)
             for c in cases:
                 _gather_check(t, hb.addr, rows, rb, np.asarray(c, dtype=np.int64))
+    hb.close()
+
+
+@pytest.mark.parametrize("rb,off", [(144, 0), (208, 16), (400, 0), (400, 48), (416, 0), (496, 32),
+                                    (512, 16), (272, 112)])
+def test_neighbour_line_sharing(rb, off):
+    """Line sharing (share=on): selected neighbours whose boundary line is fetched
+    once by the predecessor's warp. Identity, contiguous ranges (first and last row included),
+    dense shuffled and sorted selections, duplicates (several occurrences of a row and of its
+    neighbour), out-of-range indices, and the device-side-count form; forced on and off."""
+    rows = 6000
+    hb = workloads.HostBuffer(rows * rb, offset=off)
+    workloads.fill_table(hb.addr, rows, rb, 78)
+    rng = np.random.default_rng(rb + off)
+    dup = np.repeat(np.arange(200, 400), 3)
+    rng.shuffle(dup)
+    cases = [np.arange(rows), np.arange(rows)[::-1], np.arange(0, 900), np.arange(rows - 700, rows),
+             rng.permutation(rows)[:3000], np.sort(rng.choice(rows, 2500, replace=False)),
+             rng.integers(0, rows, 4000), dup, np.array([5]), np.array([rows - 1, rows - 2])]
+    bad = rng.permutation(rows)[:2000].astype(np.int64)
+    bad[[3, 700, 1999]] = [rows, -1, rows + 5]
+    bad[[10, 11]] = [bad[12] - 1 if bad[12] > 0 else 1, rows]   # a neighbour next to a bad index
+    cases.append(bad)
+    with ut.Table(hb.addr, rows, rb) as t:
+        for mode in ["share=on", "share=off"]:
+            t.set_plan(mode)
+            for c in cases:
+                _gather_check(t, hb.addr, rows, rb, np.asarray(c, dtype=np.int64))
+        t.set_plan("share=on")
+        idx = rng.permutation(rows)[:4000].astype(np.int64)
+        want, _ = oracle.gather(hb.addr, rows, rb, idx)
+        for k in [0, 1, 2500, 4000]:
+            out = torch.full((4000 * rb,), SENT, dtype=torch.uint8, device="cuda")
+            n_dev = torch.tensor([k], dtype=torch.int64, device="cuda")
+            t.gather_dn(torch.from_numpy(idx).cuda(), n_dev, out)
+            got = out.cpu().numpy()
+            assert got[:k * rb].tobytes() == want[:k * rb].tobytes()
+            assert (got[k * rb:] == SENT).all()
+    hb.close()
+
+
+def test_neighbour_line_sharing_auto_policy():
+    """auto takes line sharing for a dense selection of a 400-B table (and never below 128 B or
+    for whole-line rows), and the stats show the two launches (slot marking + gather)."""
+    rows, rb = 200_000, 400
+    hb = workloads.HostBuffer(rows * rb)
+    workloads.fill_table(hb.addr, rows, rb, 79)
+    idx = np.random.default_rng(1).permutation(rows)[:80_000].astype(np.int64)
+    with ut.Table(hb.addr, rows, rb) as t:
+        t.stats(reset=True)
+        _gather_check(t, hb.addr, rows, rb, idx)
+        assert t.stats()["kernel_launches"] == 2
+        t.set_plan("share=off")
+        t.stats(reset=True)
+        _gather_check(t, hb.addr, rows, rb, idx)
+        assert t.stats()["kernel_launches"] == 1
     hb.close()
 
 
