@@ -501,7 +501,7 @@ def run_ut(args, spec, dist):
         sampler.device_rows()          # drop the warm-up counts
 
     table.set_plan("timing=on")
-    table.stats(reset=True)
+    warm_stats = table.stats(reset=True)      # warm-up (and CUDA-graph capture) counters
     coop0 = coop.stats() if coop is not None else None
     if sampler is not None:
         sampler.mark()
@@ -545,7 +545,10 @@ def run_ut(args, spec, dist):
     own_launches = st["kernel_launches"]
     # the gather variant of the timed steps: the table's plan, "+share" when the gathers took
     # neighbour line sharing
-    plan_label = table.plan + ("+share" if st.get("share_gathers") else "")
+    # (a captured CUDA graph replays the gathers without passing through ut_gather: its capture,
+    # during warm-up, is where the choice shows)
+    shared = st.get("share_gathers") or (args.sample != "cpu" and warm_stats.get("share_gathers"))
+    plan_label = table.plan + ("+share" if shared else "")
     coop_block = None
     if coop is not None:
         c1 = coop.stats()

@@ -622,7 +622,10 @@ int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n
   cudaError_t e;
   s->rows += n;
   s->bytes += n * t->rb;
-  if (want_share(t, p, n)) return gather_share(t, s, a, st);
+  if (want_share(t, p, n)) {
+    const int rc = gather_share(t, s, a, st);
+    if (rc != UT_ENOMEM) return rc;          // no room for the slot array: the plain gather below
+  }
   const bool runs = want_runs(t, p, n);
   if (!runs && (!want_reorder(t, n) || p.kind == P_PAPER_NAIVE || p.kind == P_PAPER_SHIFT ||
                 p.kind == P_TMA4)) {
@@ -816,8 +819,10 @@ bool want_share(const ut_table* t, const Plan& p, uint64_t n) {
 int gather_share(const ut_table* t, DevState* s, const ut::GatherArgs& a, cudaStream_t st) {
   uint32_t* slot = nullptr;
   cudaError_t e;
-  if ((e = cudaMallocFromPoolAsync((void**)&slot, t->rows * sizeof(uint32_t), s->pool, st)) != cudaSuccess)
-    return cuda_err(e, "cudaMallocFromPoolAsync(share slots)");
+  if ((e = cudaMallocFromPoolAsync((void**)&slot, t->rows * sizeof(uint32_t), s->pool, st)) != cudaSuccess) {
+    cudaGetLastError();
+    return UT_ENOMEM;
+  }
   e = cudaMemsetAsync(slot, 0, t->rows * sizeof(uint32_t), st);
   if (e == cudaSuccess) {
     const int gm = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)s->sms * 8, (a.n + 255) / 256));
