@@ -102,3 +102,28 @@ def test_plan_depends_on_output_alignment():
     assert ut.ut_plan_probe(0x10000, 10, 400, 0x20000) == "vec16.g32"
     assert ut.ut_plan_probe(0x10000, 10, 400, 0x20004) == "realign.g32"
     assert ut.ut_plan_probe(0x10000, 10, 4, 0x20002) == "realign.g2"
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    """The ctypes mirrors of ut_stats, ut_table_info and ut_coop_stats have the C structs' size
+    and field offsets (compiled from include/ut.h by gcc)."""
+    mirrors = {"ut_stats": ut._Stats, "ut_table_info": ut._Info, "ut_coop_stats": ut._CoopStats}
+    lines = ["#include <stddef.h>", "#include <stdio.h>", '#include "ut.h"', "int main(void) {"]
+    for cname, py in mirrors.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'  printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+                    "-o", str(exe), str(src)], check=True)
+    got = {}
+    for l in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        c, f, v = l.split()
+        got[(c, f)] = int(v)
+    for cname, py in mirrors.items():
+        assert got[(cname, "size")] == ctypes.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert got[(cname, f)] == getattr(py, f).offset, (cname, f)
