@@ -627,8 +627,9 @@ int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n
     if (rc != UT_ENOMEM) return rc;          // no room for the slot array: the plain gather below
   }
   const bool runs = want_runs(t, p, n);
+  // (the reorder splits gathers into 2^31-row chunks, which a device-side row count cannot follow)
   if (!runs && (!want_reorder(t, n) || p.kind == P_PAPER_NAIVE || p.kind == P_PAPER_SHIFT ||
-                p.kind == P_TMA4)) {
+                p.kind == P_TMA4 || (n_dev && n > (1ull << 31)))) {
     if (host_out && want_stage(t, (uint64_t)out_dev, p)) {
       e = timed(t, s, st, [&] { return launch_staged(t, s, st, a); });
       if (e != cudaSuccess) return cuda_err(e, "staged gather");
@@ -643,6 +644,14 @@ int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n
   // library's pool); n < 2^32 per launch, larger gathers are split.
   const int shift = bucket_shift(t->bytes, t->rb);
   const uint32_t nb = (uint32_t)(((t->bytes - 1) >> shift) + 1);
+  const int hsm = (int)(nb * sizeof(uint32_t));
+  static const bool smem_ok = [] {
+    const int mx = ut::kMaxBuckets * (int)sizeof(uint32_t);
+    return cudaFuncSetAttribute(ut::k_bucket_count, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess &&
+           cudaFuncSetAttribute(ut::k_bucket_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess &&
+           cudaFuncSetAttribute(ut::k_bucket_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess;
+  }();
+  if (!smem_ok) return set_err(UT_ECUDA, "cannot opt in to %d B of shared memory", hsm);
   const uint64_t chunk = 1ull << 31;
   for (uint64_t off = 0; off < n; off += chunk) {
     const uint64_t cnt_n = std::min(chunk, n - off);
@@ -659,16 +668,10 @@ int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n
     c.perm = perm;
     const uint64_t blocks = std::min<uint64_t>((uint64_t)s->sms * 2, (cnt_n + 2047) / 2048);
     const uint64_t per_block = (cnt_n + blocks - 1) / blocks;
-    if ((e = cudaMemsetAsync(cnt, 0, nb * sizeof(uint32_t), st)) != cudaSuccess)
+    if ((e = cudaMemsetAsync(cnt, 0, nb * sizeof(uint32_t), st)) != cudaSuccess) {
+      cudaFreeAsync(scratch, st);
       return cuda_err(e, "cudaMemsetAsync(buckets)");
-    const int hsm = (int)(nb * sizeof(uint32_t));
-    static const bool smem_ok = [] {
-      const int mx = ut::kMaxBuckets * (int)sizeof(uint32_t);
-      return cudaFuncSetAttribute(ut::k_bucket_count, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess &&
-             cudaFuncSetAttribute(ut::k_bucket_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess &&
-             cudaFuncSetAttribute(ut::k_bucket_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess;
-    }();
-    if (!smem_ok) return set_err(UT_ECUDA, "cannot opt in to %d B of shared memory", hsm);
+    }
     ut::k_bucket_count<<<(int)blocks, 512, hsm, st>>>(c, shift, nb, per_block, cnt);
     ut::k_bucket_scan<<<1, 1024, hsm, st>>>(cnt, nb);
     ut::k_bucket_scatter<<<(int)blocks, 512, hsm, st>>>(c, shift, nb, per_block, cnt, perm);
@@ -753,6 +756,14 @@ int gather_runs(const ut_table* t, DevState* s, const Plan& p, const ut::GatherA
   // scratch (uint32 words): cnt[nb], perm[n], flags[n], pos[n], starts[n+1], sums[tiles],
   // then two 8-byte words: the effective n and the run count
   const size_t words = (size_t)nb + 4 * n + 1 + tiles + 6;
+  const int hsm = (int)(nb * sizeof(uint32_t));
+  static const bool smem_ok = [] {
+    const int mx = ut::kMaxBuckets * (int)sizeof(uint32_t);
+    return cudaFuncSetAttribute(ut::k_bucket_count, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess &&
+           cudaFuncSetAttribute(ut::k_bucket_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess &&
+           cudaFuncSetAttribute(ut::k_bucket_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess;
+  }();
+  if (!smem_ok) return set_err(UT_ECUDA, "cannot opt in to %d B of shared memory", hsm);
   uint32_t* scratch = nullptr;
   cudaError_t e;
   if ((e = cudaMallocFromPoolAsync((void**)&scratch, words * sizeof(uint32_t), s->pool, st)) != cudaSuccess)
@@ -770,17 +781,13 @@ int gather_runs(const ut_table* t, DevState* s, const Plan& p, const ut::GatherA
   a.perm = perm;
   const uint64_t blocks = std::min<uint64_t>((uint64_t)s->sms * 2, (n + 2047) / 2048);
   const uint64_t per_block = (n + blocks - 1) / blocks;
-  const int hsm = (int)(nb * sizeof(uint32_t));
-  static const bool smem_ok = [] {
-    const int mx = ut::kMaxBuckets * (int)sizeof(uint32_t);
-    return cudaFuncSetAttribute(ut::k_bucket_count, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess &&
-           cudaFuncSetAttribute(ut::k_bucket_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess &&
-           cudaFuncSetAttribute(ut::k_bucket_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) == cudaSuccess;
-  }();
-  if (!smem_ok) return set_err(UT_ECUDA, "cannot opt in to %d B of shared memory", hsm);
   const int gb = (int)((n + 255) / 256);
   ut::k_eff_n<<<1, 1, 0, st>>>(a0.n_dev, n, n_eff);
-  cudaMemsetAsync(cnt, 0, nb * sizeof(uint32_t), st);
+  e = cudaMemsetAsync(cnt, 0, nb * sizeof(uint32_t), st);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(scratch, st);
+    return cuda_err(e, "cudaMemsetAsync(run buckets)");
+  }
   ut::k_bucket_count<<<(int)blocks, 512, hsm, st>>>(a, shift, nb, per_block, cnt);
   ut::k_bucket_scan<<<1, 1024, hsm, st>>>(cnt, nb);
   ut::k_bucket_scatter<<<(int)blocks, 512, hsm, st>>>(a, shift, nb, per_block, cnt, perm);
