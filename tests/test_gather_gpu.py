@@ -329,10 +329,17 @@ def test_neighbour_line_sharing_auto_policy():
         t.stats(reset=True)
         _gather_check(t, hb.addr, rows, rb, idx)
         assert t.stats()["kernel_launches"] == 2
+        # the end-to-end form (pinned host output: direct stores) takes it too
+        want, _ = oracle.gather(hb.addr, rows, rb, idx)
+        t.stats(reset=True)
+        got = t.gather_host(torch.from_numpy(idx).pin_memory())
+        assert got.numpy().tobytes() == want.tobytes()
+        assert t.stats()["share_gathers"] == 1
         t.set_plan("share=off")
         t.stats(reset=True)
         _gather_check(t, hb.addr, rows, rb, idx)
         assert t.stats()["kernel_launches"] == 1
+        assert t.stats()["share_gathers"] == 0
     hb.close()
 
 
