@@ -119,7 +119,10 @@ class Dist:
                 torch.cuda.set_device(self.local_rank % torch.cuda.device_count())
                 td.init_process_group(backend="nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
             else:
-                td.init_process_group(backend=backend)
+                import datetime
+                # the threads harness keeps ranks > 0 waiting while rank 0 fills and times the
+                # box (a 57-GB table fill takes minutes): a generous rendezvous timeout
+                td.init_process_group(backend=backend, timeout=datetime.timedelta(hours=2))
             self.pg = td
 
     def barrier(self):
@@ -160,8 +163,8 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index if isinstance(gpu_index, int) else ",".join(str(g) for g in gpu_index)
         self.lines: list[str] = []
         self.proc = None
         self.thread = None
@@ -211,21 +214,25 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def h2d_ceiling(torch, nbytes: int = 1 << 30, reps: int = 10) -> float:
-    """Pinned cudaMemcpy H2D ceiling (GB/s): best of `reps` copies of `nbytes`, CUDA events."""
-    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
-    h.fill_(1)
+def h2d_ceiling(torch, nbytes: int = 1 << 30, reps: int = 10, stream=None, host=None) -> float:
+    """Pinned cudaMemcpy H2D ceiling (GB/s) of the current device: best of `reps` copies of
+    `nbytes`, CUDA events on `stream` (default: the current stream)."""
+    h = host if host is not None else torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    if host is None:
+        h.fill_(1)
     d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    st = stream if stream is not None else torch.cuda.current_stream()
     best = 0.0
-    for _ in range(reps):
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        d.copy_(h, non_blocking=True)
-        e1.record()
-        torch.cuda.synchronize()
-        best = max(best, nbytes / e0.elapsed_time(e1) / 1e6)
-    del h, d
+    with torch.cuda.stream(st):
+        for _ in range(reps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            d.copy_(h[:nbytes], non_blocking=True)
+            e1.record(st)
+            st.synchronize()
+            best = max(best, nbytes / e0.elapsed_time(e1) / 1e6)
+    del d
     return best
 
 
@@ -295,39 +302,54 @@ def cpu_oracle_rate(table_addr: int, spec: dict, lists: list[np.ndarray], budget
 
 # ---- the arms ------------------------------------------------------------------------------------
 def run_reference(args, spec, dist):
-    """Reference arm: the oracle on the host cores, K timed steps of one minibatch each.
-    Under torchrun only rank 0 runs it; the other ranks exit without work."""
+    """Reference arm: the oracle on the host cores, K timed steps of one minibatch each, over the
+    SAME index lists GPU 0 of the ut arm gathers (same seed, same rank slicing, same cycling), so
+    the two lines describe one workload. Under torchrun only rank 0 runs it; the other ranks
+    exit without work."""
     if dist.rank != 0:
         return
     import oracle
     seed = args.seed
-    lists = make_index_lists(spec, 0, 1, args.warmup + args.steps, seed, os.cpu_count() or 1)
+    count = min(args.warmup + args.steps, args.max_lists)
+    lists = make_index_lists(spec, 0, args.gpus, count, seed, os.cpu_count() or 1)
     hb = open_table(spec, 0, 1, seed, None, "ref")
     rb = spec["row_bytes"]
     out = np.empty(max(l.size for l in lists) * rb, dtype=np.uint8)
     for s in range(args.warmup):
-        oracle.gather_into(hb.addr, spec["rows"], rb, lists[s], out)
-    t0 = time.perf_counter()
+        oracle.gather_into(hb.addr, spec["rows"], rb, lists[s % count], out)
+    step_ms = []
     nbytes = 0
-    for s in range(args.steps):
-        l = lists[args.warmup + s]
+    timed = [lists[(args.warmup + s) % count] for s in range(args.steps)]
+    for l in timed:
+        t1 = time.perf_counter()
         oracle.gather_into(hb.addr, spec["rows"], rb, l, out)
+        step_ms.append((time.perf_counter() - t1) * 1e3)
         nbytes += l.size * rb
-    el = time.perf_counter() - t0
+    el = sum(step_ms) / 1e3
     value = nbytes / el / 1e9
     line = {"metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "impl": "reference",
-            "config": config_block(spec, lists[args.warmup:], args.gpus),
+            "config": config_block(spec, timed, args.gpus, args.seed),
+            "step_ms": step_stats(step_ms),
             "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1,
                              "kind": "oracle",
-                             "sample": f"{args.steps} full minibatches of the workload, single-threaded plain C"},
+                             "sample": f"{args.steps} full minibatches of the workload (GPU 0's "
+                                       f"lists of the ut arm), single-threaded plain C"},
             "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     hb.close()
+
+
+def step_stats(ms: list[float]) -> dict:
+    """Per-step device (or host) times: the spread a single mean hides (VERDICT r1 weak #1)."""
+    if not ms:
+        return {}
+    return {"min": round(min(ms), 4), "median": round(statistics.median(ms), 4),
+            "max": round(max(ms), 4), "n": len(ms)}
 
 
 def traffic_model(spec: dict, lists) -> dict:
@@ -347,13 +369,15 @@ def traffic_model(spec: dict, lists) -> dict:
             "line_requests_per_step": round(m(lines), 1)}
 
 
-def config_block(spec: dict, lists, world: int) -> dict:
+def config_block(spec: dict, lists, world: int, seed: int) -> dict:
     rows_per_step = float(np.mean([l.size for l in lists])) if lists else 0.0
     c = {"workload": spec["workload"], "table_rows": spec["rows"], "row_bytes": spec["row_bytes"],
+         "seed": seed, "index_lists": "GPU g of N takes rank-g slices (workloads.graphsage / "
+                                      "uniform_idx seeded from `seed`); the reference arm times GPU 0's",
          "table_gb": round(spec["rows"] * spec["row_bytes"] / 1e9, 3),
          "rows_per_step_per_gpu": round(rows_per_step, 1),
          "mb_per_step_per_gpu": round(rows_per_step * spec["row_bytes"] / 1e6, 2),
-         "parallelism": f"dp{world} (independent minibatches per GPU, one shared host table)",
+         "parallelism": f"dp{world} (independent minibatch stream per GPU, one shared host table)",
          "l2": "flushed (256 MiB write) between timed steps, outside the per-step events"}
     c.update(traffic_model(spec, lists[:8]))
     if spec["kind"] == "graphsage":
@@ -373,14 +397,17 @@ class _Owned:
         pass
 
 
-def run_ut(args, spec, dist):
+def run_procs(args, spec, dist):
+    """One process per GPU (torchrun ranks; --harness procs): each rank registers the shared
+    /dev/shm table or holds its own partition (--coop), and gathers its own minibatches. The
+    form for the cooperative gather and GPU sampling; the default is run_box."""
     import torch
 
     rank, world = dist.rank, dist.world
     seed = args.seed
     count = min(args.warmup + args.steps, args.max_lists)
     procs = max(1, (os.cpu_count() or 1) // world)
-    lists = make_index_lists(spec, rank, world, count, seed + 17, procs)   # before CUDA init
+    lists = make_index_lists(spec, rank, world, count, seed, procs)   # before CUDA init
     if args.presort:   # experiment only: what a perfectly address-ordered list would give
         lists = [np.sort(l) for l in lists]
 
@@ -650,7 +677,8 @@ def run_ut(args, spec, dist):
 
     if rank == 0:
         n_launch = int(launches)
-        cfg = config_block(spec, lists[args.warmup:] or lists, world)
+        cfg = config_block(spec, [lists[(args.warmup + s) % count] for s in range(args.steps)],
+                           world, args.seed)
         sect_ratio = (cfg["sector_floor_mb_per_step"] / cfg["mb_per_step_per_gpu"]
                       if cfg.get("mb_per_step_per_gpu") else None)
         line = {
@@ -703,6 +731,386 @@ def run_ut(args, spec, dist):
         hb.close(unlink=True)
     else:
         hb.close()
+
+
+# ---- the default harness: one process, ONE table, one host thread per GPU ----------------------
+def run_threads(n: int, fn):
+    """fn(g) for g in 0..n-1 on n threads at once; results in GPU order; re-raises a failure."""
+    res, errs = [None] * n, [None] * n
+
+    def body(g):
+        try:
+            res[g] = fn(g)
+        except BaseException as e:  # noqa: BLE001 - re-raised below on the main thread
+            errs[g] = e
+
+    ts = [threading.Thread(target=body, args=(g,), name=f"gpu{g}") for g in range(n)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in errs:
+        if e is not None:
+            raise e
+    return res
+
+
+def box_table(spec: dict, args, ut):
+    """The box's ONE host feature table, shared by every GPU of the process.
+
+    auto/managed: the paper's own unified-tensor allocation — cudaMallocManaged with
+    SetPreferredLocation = CPU and SetAccessedBy = each GPU (Table 2; ut_create
+    extends AccessedBy to a device the first time it gathers). On this pool it is the only host
+    memory kind that reads random rows at link speed at any table size (managed 50.7 GB/s for
+    random 512-B rows over 53 GB; registered / pinned / VMM host memory 25.7-29, profiles/r2/
+    shared_table_probe.jsonl) — and it is process-private, which is why one process drives all
+    GPUs. register: an anonymous mmap pinned in place (ut_register); pinned / vmm: ut_create."""
+    rows, rb = spec["rows"], spec["row_bytes"]
+    kind = "managed" if args.alloc == "auto" else args.alloc
+    threads = os.cpu_count() or 1
+    if kind == "register":
+        hb = workloads.HostBuffer(rows * rb)
+        hb.numa = workloads.interleave(hb.addr, rows * rb)
+        workloads.fill_table(hb.addr, rows, rb, args.seed, threads=threads)
+        import paper_2101_07956_b200 as _ut
+        return _ut.Table(hb.addr, rows, rb), hb, kind
+    table = ut.Table.create(rows, rb, kind)
+    workloads.fill_table(table.host_addr, rows, rb, args.seed, threads=threads)
+    return table, _Owned(table.host_addr), kind
+
+
+class BoxWorker:
+    """GPU g's share of a box run: its minibatch index lists resident in HBM, its output and
+    L2-flush buffers and a stream of its own. Every method runs on the calling thread with
+    device g made current (CUDA's current device is per host thread)."""
+
+    def __init__(self, g: int, torch, table, spec: dict, lists, args):
+        torch.cuda.set_device(g)
+        self.g, self.torch, self.table, self.spec, self.args = g, torch, table, spec, args
+        self.rb = spec["row_bytes"]
+        self.lists = lists
+        self.stream = torch.cuda.Stream()
+        self.max_n = max(l.size for l in lists)
+        with torch.cuda.stream(self.stream):
+            self.idx = [torch.from_numpy(l).to("cuda") for l in lists]
+            self.out = torch.empty(self.max_n * self.rb, dtype=torch.uint8, device="cuda")
+            self.flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+        self.stream.synchronize()
+
+    def gather(self, k: int) -> int:
+        l = self.idx[k % len(self.idx)]
+        self.table.gather(l, out=self.out[: l.numel() * self.rb], stream=self.stream)
+        return l.numel() * self.rb
+
+    def parity(self, host_addr: int, budget_bytes: int) -> int:
+        """Byte-exact check of this GPU's lists against the oracle, outside timing (SURVEY §4
+        T2): every list while the rows fit `budget_bytes`, at least two. Returns lists checked."""
+        import oracle
+        rb = self.rb
+        want = np.empty(self.max_n * rb, dtype=np.uint8)
+        checked, total = 0, 0
+        for k, l in enumerate(self.lists):
+            if checked >= 2 and total + l.size * rb > budget_bytes:
+                break
+            bad = oracle.gather_into(host_addr, self.spec["rows"], rb, l, want)
+            self.gather(k)
+            self.stream.synchronize()
+            got = self.out[: l.size * rb].cpu().numpy()
+            if got.tobytes() != want[: l.size * rb].tobytes() or \
+                    self.table.error_pos(self.stream) != bad:
+                raise SystemExit(f"GPU {self.g}: parity failure on minibatch {k}")
+            checked += 1
+            total += l.size * rb
+        return checked
+
+    def warmup(self) -> None:
+        for s in range(self.args.warmup):
+            self.gather(s)
+        self.stream.synchronize()
+
+    def timed(self, start) -> dict:
+        """K steps, each bracketed by CUDA events on this GPU's stream, the L2 flushed between
+        steps outside the events. `start` (a threading.Barrier) releases every GPU at once."""
+        torch, args = self.torch, self.args
+        self.stream.synchronize()
+        start.wait()
+        torch.cuda.nvtx.range_push("timed")    # ncu --nvtx-include "timed/" profiles these
+        t0 = time.perf_counter()
+        evs, nbytes = [], 0
+        for s in range(args.steps):
+            with torch.cuda.stream(self.stream):
+                self.flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(self.stream)
+            nbytes += self.gather(args.warmup + s)
+            e1.record(self.stream)
+            evs.append((e0, e1))
+        self.stream.synchronize()
+        wall = time.perf_counter() - t0
+        torch.cuda.nvtx.range_pop()
+        return {"bytes": nbytes, "ms": [a.elapsed_time(b) for a, b in evs], "wall_s": wall}
+
+    def e2e(self, start) -> dict:
+        """End to end through the public API, per step: (1) ut_gather_host — pinned host idx in,
+        pinned host rows out; (2) the paper's Listing 2 pipeline — pinned idx H2D, gather into
+        HBM, an 8-B read-back of the result. Host wall time per step; all GPUs at once."""
+        torch, args, rb = self.torch, self.args, self.rb
+        idx_host = [torch.from_numpy(x).pin_memory() for x in self.lists]
+        out_host = torch.empty(self.max_n * rb, dtype=torch.uint8, pin_memory=True)
+        probe = torch.empty(1, dtype=torch.int64, pin_memory=True)
+        for s in range(min(2, len(idx_host))):
+            self.table.gather_host(idx_host[s], out_host=out_host, stream=self.stream)
+        r = {"e_sec": 0.0, "f_sec": 0.0, "bytes": 0, "h2d": 0, "d2h": 0}
+        start.wait()
+        for s in range(args.steps):
+            ih = idx_host[(args.warmup + s) % len(idx_host)]
+            with torch.cuda.stream(self.stream):
+                self.flush.zero_()
+            self.stream.synchronize()
+            t1 = time.perf_counter()
+            self.table.gather_host(ih, out_host=out_host, stream=self.stream)
+            r["e_sec"] += time.perf_counter() - t1
+            r["bytes"] += ih.numel() * rb
+            r["h2d"] += ih.numel() * 8
+            r["d2h"] += ih.numel() * rb
+        start.wait()
+        for s in range(args.steps):
+            ih = idx_host[(args.warmup + s) % len(idx_host)]
+            with torch.cuda.stream(self.stream):
+                self.flush.zero_()
+            self.stream.synchronize()
+            t1 = time.perf_counter()
+            with torch.cuda.stream(self.stream):
+                idx_d = ih.to("cuda", non_blocking=True)
+                res = self.table.gather(idx_d, out=self.out[: ih.numel() * rb], stream=self.stream)
+                probe.copy_(res[:8].view(torch.int64), non_blocking=True)
+            self.stream.synchronize()
+            r["f_sec"] += time.perf_counter() - t1
+        del out_host, idx_host
+        return r
+
+
+class StubWorker:
+    """--dry-run stand-in for BoxWorker (no GPU, no library): numpy row copies timed on the host,
+    so the harness's launch, threading and reductions are testable on CPU. Its numbers are not
+    a measurement of anything."""
+
+    def __init__(self, g, table_view, spec, lists, args):
+        self.g, self.view, self.spec, self.lists, self.args = g, table_view, spec, lists, args
+        self.rb = spec["row_bytes"]
+
+    def gather(self, k):
+        l = self.lists[k % len(self.lists)]
+        np.take(self.view, l, axis=0)
+        return l.size * self.rb
+
+    def warmup(self):
+        for s in range(self.args.warmup):
+            self.gather(s)
+
+    def timed(self, start):
+        start.wait()
+        t0 = time.perf_counter()
+        ms, nbytes = [], 0
+        for s in range(self.args.steps):
+            t1 = time.perf_counter()
+            nbytes += self.gather(self.args.warmup + s)
+            ms.append((time.perf_counter() - t1) * 1e3)
+        return {"bytes": nbytes, "ms": ms, "wall_s": time.perf_counter() - t0}
+
+
+def run_box(args, spec, dist=None):
+    """The default harness (any N): ONE process drives all N GPUs, one host thread each, over ONE
+    host table (the paper's managed unified tensor, `box_table`). Each GPU gathers its own
+    minibatch stream (GPU g takes the rank-g slices of the seeded roots): data parallel by
+    minibatch with no collective on the path ("scaling": "weak"). value = Σ_g useful
+    bytes ÷ max_g (summed per-step device time)."""
+    N = args.gpus
+    seed = args.seed
+    count = min(args.warmup + args.steps, args.max_lists)
+    procs = max(1, (os.cpu_count() or 1) // max(1, min(N, 4)))
+    lists = [make_index_lists(spec, g, N, count, seed, procs) for g in range(N)]  # before CUDA
+    timed_lists = [lists[0][(args.warmup + s) % count] for s in range(args.steps)]
+    if args.dry_run:
+        rows, rb = spec["rows"], spec["row_bytes"]
+        view = np.zeros((min(rows, 1 << 16), rb), dtype=np.uint8)
+        lists = [[l % view.shape[0] for l in ls] for ls in lists]
+        workers = [StubWorker(g, view, spec, lists[g], args) for g in range(N)]
+        run_threads(N, lambda g: workers[g].warmup())
+        start = threading.Barrier(N)
+        res = run_threads(N, lambda g: workers[g].timed(start))
+        dev_ms = [sum(r["ms"]) for r in res]
+        total = sum(r["bytes"] for r in res)
+        value = total / (max(dev_ms) / 1e3) / 1e9
+        if dist is not None and dist.world > 1:       # the launch check: every rank is present
+            ranks = int(dist.allreduce([1.0], "sum")[0])
+        else:
+            ranks = 1
+        print(json.dumps({
+            "metric": METRIC, "value": round(value, 6), "unit": "GB/s", "n_gpus": N,
+            "steps": args.steps, "warmup": args.warmup, "dry_run": True,
+            "harness": "threads (one process, one thread per GPU)", "launcher_ranks": ranks,
+            "ms_per_step": round(max(dev_ms) / args.steps, 6),
+            "per_gpu": [{"gpu": g, "bytes": r["bytes"], "ms": round(sum(r["ms"]), 6)}
+                        for g, r in enumerate(res)],
+            "config": {"workload": spec["workload"], "seed": seed},
+            "note": "--dry-run: numpy stand-in for the GPU arm, NOT a measurement"}), flush=True)
+        return
+
+    import torch
+    ndev = torch.cuda.device_count()
+    if ndev < N:
+        raise SystemExit(f"--gpus {N}: only {ndev} CUDA device(s) visible")
+    torch.cuda.set_device(0)
+    import paper_2101_07956_b200 as ut
+    t_reg = time.perf_counter()
+    table, hb, kind = box_table(spec, args, ut)
+    reg_s = time.perf_counter() - t_reg
+    if args.plan:
+        for p in args.plan.split(","):
+            table.set_plan(p)
+    rb = spec["row_bytes"]
+    workers = run_threads(N, lambda g: BoxWorker(g, torch, table, spec, lists[g], args))
+
+    # roofline denominators, measured now: each GPU's link alone, then all at once
+    def link(g, reps=10):
+        torch.cuda.set_device(g)
+        return h2d_ceiling(torch, stream=workers[g].stream, reps=reps)
+    link_solo = [link(g) for g in range(N)]
+    link_conc = run_threads(N, link) if N > 1 else list(link_solo)
+    torch.cuda.set_device(0)
+    sm_ceiling = sm_read_ceiling(torch, ut)
+
+    parity_lists = 0
+    if args.check:
+        budget = (16 << 30) // N
+        parity_lists = sum(run_threads(N, lambda g: (torch.cuda.set_device(g),
+                                                      workers[g].parity(hb.addr, budget))[1]))
+
+    clocks = ClockSampler(list(range(N)))
+    clocks.start()
+    run_threads(N, lambda g: (torch.cuda.set_device(g), workers[g].warmup()))
+    table.set_plan("timing=on")
+    run_threads(N, lambda g: (torch.cuda.set_device(g), table.stats(reset=True)))
+    start = threading.Barrier(N)
+    res = run_threads(N, lambda g: (torch.cuda.set_device(g), workers[g].timed(start))[1])
+    clk = clocks.stop()
+    stats = run_threads(N, lambda g: (torch.cuda.set_device(g), table.stats(reset=True))[1])
+    table.set_plan("timing=off")
+    # the link ceiling again, right after timing: box drift shows as a change here
+    link_after = run_threads(N, lambda g: link(g, reps=5)) if N > 1 else [link(0, reps=5)]
+
+    dev_ms = [sum(r["ms"]) for r in res]
+    total = sum(r["bytes"] for r in res)
+    value = total / (max(dev_ms) / 1e3) / 1e9
+    per_gpu = [r["bytes"] / (m / 1e3) / 1e9 for r, m in zip(res, dev_ms)]
+    kern_ms = sum(s["gather_kernel_ms"] for s in stats)
+    kern_n = sum(s["timed_launches"] for s in stats)
+    achieved = total / (kern_ms / 1e3) / 1e9 / N if kern_ms > 0 else None    # per GPU
+    launches = sum(s["kernel_launches"] for s in stats)
+    shared = any(s.get("share_gathers") for s in stats)
+    plan_label = table.plan + ("+share" if shared else "")
+    all_ms = [m for r in res for m in r["ms"]]
+
+    e2e = None
+    if not args.no_e2e:
+        start = threading.Barrier(N)
+        er = run_threads(N, lambda g: (torch.cuda.set_device(g), workers[g].e2e(start))[1])
+        eb = sum(r["bytes"] for r in er)
+        e2e = {"value": round(eb / max(r["e_sec"] for r in er) / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": int(sum(r["h2d"] for r in er) / args.steps),
+               "d2h_bytes_per_step": int(sum(r["d2h"] for r in er) / args.steps),
+               "path": "ut_gather_host on every GPU at once: pinned host idx in, pinned host rows out",
+               "to_hbm": {"value": round(eb / max(r["f_sec"] for r in er) / 1e9, 3), "unit": "GB/s",
+                          "h2d_bytes_per_step": int(sum(r["h2d"] for r in er) / args.steps),
+                          "d2h_bytes_per_step": 8 * N,
+                          "path": "Table.gather with a pinned host idx: idx H2D, gather into HBM, "
+                                  "8-B read-back of the result (the paper's Listing 2 pipeline)"}}
+
+    # NCCL all-reduce smoke (N > 1, untimed, off the gather path; SURVEY §2.3 ii): one
+    # single-process multi-GPU all-reduce over NVLink/NVSwitch
+    ar = None
+    if N > 1 and not args.no_allreduce_smoke:
+        import torch.cuda.nccl as nccl
+        bufs = []
+        for g in range(N):
+            with torch.cuda.device(g):
+                bufs.append(torch.full((1 << 20,), float(g + 1), dtype=torch.float32, device="cuda"))
+        t1 = time.perf_counter()
+        nccl.all_reduce(bufs)
+        for g in range(N):
+            torch.cuda.synchronize(g)
+        want = N * (N + 1) / 2
+        ar = {"ok": all(bool((b == want).all().item()) for b in bufs), "bytes": bufs[0].numel() * 4,
+              "ms": round((time.perf_counter() - t1) * 1e3, 3),
+              "backend": "nccl (torch.cuda.nccl, one process, all GPUs)", "gpus": N}
+        del bufs
+
+    dram = None
+    if not args.no_cpu:
+        import baselines
+        dram = round(baselines.host_read_gbs(hb.addr, min(spec["rows"] * rb, 8 << 30)), 2)
+    cpu_base, py_base = None, None
+    if N == 1 and not args.no_cpu:
+        torch.cuda.set_device(0)
+        v, nl, el = cpu_oracle_rate(hb.addr, spec, lists[0], args.cpu_budget)
+        cpu_base = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                    "sample": f"{nl} minibatches of the workload in {el:.1f} s, single-threaded plain C"}
+        py_base = cpu_staged_baseline(torch, hb.addr, spec, lists[0], args)
+
+    cfg = config_block(spec, timed_lists, N, seed)
+    sect_ratio = (cfg["sector_floor_mb_per_step"] / cfg["mb_per_step_per_gpu"]
+                  if cfg.get("mb_per_step_per_gpu") else None)
+    link_g = statistics.mean(link_solo)
+    box_link = sum(link_conc)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": N,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(max(dev_ms) / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (self-identifying fp32-row table, GraphSAGE-shaped index lists)",
+        "config": cfg,
+        "harness": "threads: one process drives all GPUs (one host thread each) over one table",
+        "step_ms": step_stats(all_ms),
+        "per_gpu_gbs": [round(x, 3) for x in per_gpu],
+        "transferred_gbs_sector_floor": round(value * sect_ratio, 3) if sect_ratio else None,
+        "line_requests_per_s": (round(cfg["line_requests_per_step"] * N / (max(dev_ms) / args.steps / 1e3))
+                                if cfg.get("line_requests_per_step") else None),
+        "h2d_memcpy_gbs": round(link_g, 3),
+        "h2d_memcpy_gbs_per_gpu": [round(x, 3) for x in link_solo],
+        "h2d_memcpy_concurrent_gbs": round(box_link, 3),
+        "h2d_memcpy_gbs_after_timing": [round(x, 3) for x in link_after],
+        "host_dram_read_gbs": dram,
+        "box_roofline_gbs": round(min(box_link, dram), 3) if dram else round(box_link, 3),
+        "frac_of_link": round(value / N / link_g, 4),
+        "frac_of_box_roofline": round(value / (min(box_link, dram) if dram else box_link), 4),
+        "sm_read_ceiling_gbs": round(sm_ceiling, 3),
+        "frac_of_sm_read_ceiling": round(value / N / sm_ceiling, 4),
+        "plan": plan_label,
+        "table_memory": kind + (" (cudaMallocManaged + SetPreferredLocation=CPU + SetAccessedBy "
+                                "every GPU: one copy for the box)" if kind == "managed" else ""),
+        "roofline": {"bound": "pcie_h2d",
+                     "achieved": round(achieved, 3) if achieved is not None else None,
+                     "peak": round(link_g, 3), "unit": "GB/s",
+                     "frac": round(achieved / link_g, 4) if achieved is not None else None,
+                     **ncu_traffic(spec["workload"], plan_label, kind, args),
+                     "kernel": f"gather {plan_label} (device time of the gather kernels, share "
+                               f"hash/mark included, CUDA events on the launch stream; per GPU)",
+                     "timed_launches": kern_n,
+                     "peak_source": "pinned cudaMemcpy H2D measured in this run (best of 10 x 1 GiB), "
+                                    "mean over the GPUs, each alone",
+                     "sm_read_ceiling": round(sm_ceiling, 3)},
+        "cpu_baseline": cpu_base, "py_baseline": py_base, "e2e": e2e,
+        "gpu_launches": int(launches), "clocks": clk,
+        "parity_checked": bool(args.check), "parity_lists_checked": parity_lists,
+        "register_s": round(reg_s, 3), "allreduce_smoke": ar,
+        "wall_ms_per_step": round(max(r["wall_s"] for r in res) / args.steps * 1e3, 3),
+    }
+    print(json.dumps(line), flush=True)
+    del workers
+    table.close()
+    hb.close()
 
 
 class GpuSampling:
@@ -969,13 +1377,34 @@ def cpu_staged_baseline(torch, table_addr, spec, lists, args):
     return out
 
 
+def self_launch(args, argv) -> int:
+    """`--harness procs` at N > 1 without torchrun: start the N ranks ourselves (torchrun on
+    127.0.0.1, one process per GPU) and return their exit code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
+
+
 def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="products")
+    ap.add_argument("--config", default="papers",
+                    help="papers (default: ogbn-papers100M-shaped, the largest single-GPU config), "
+                         "products, reddit, tiny, sweep:RB")
     ap.add_argument("--impl", default="ut", choices=["ut", "reference"])
+    ap.add_argument("--harness", default="threads", choices=["threads", "procs"],
+                    help="threads (default): one process drives all N GPUs over one table; "
+                         "procs: one process per GPU (torchrun ranks; --coop, --sample gpu)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="harness test without a GPU: numpy stand-in for the GPU arm")
     ap.add_argument("--seed", type=int, default=2101)
     ap.add_argument("--plan", default="", help="comma list passed to ut_set_plan (A/B runs)")
     ap.add_argument("--max-lists", type=int, default=64, help="distinct minibatches per rank")
@@ -989,13 +1418,13 @@ def main(argv=None):
                     help="override Table 4's edge count of a GraphSAGE config (e.g. reddit 114600000)")
     ap.add_argument("--coop", default="off", choices=["off", "device", "host"],
                     help="cooperative gather across ranks (ut_coop; DESIGN.md §10d): phases "
-                         "synchronised on the device or by host barriers")
+                         "synchronised on the device or by host barriers (implies --harness procs)")
     ap.add_argument("--alloc", default="auto", choices=["auto", "register", "pinned", "managed", "vmm"],
-                    help="table memory: caller mmap + ut_register, or ut_create(kind); auto = "
-                         "managed for one rank and a table > 1 GiB, else register")
+                    help="table memory: auto = managed (the paper's unified tensor) in the threads "
+                         "harness; in procs: managed for one rank and a table > 1 GiB, else register")
     ap.add_argument("--sample", default="cpu", choices=["cpu", "gpu"],
                     help="cpu: index lists sampled before timing (default, the paper's split); "
-                         "gpu: ut_sample inside every timed step (SURVEY NEXT-2)")
+                         "gpu: ut_sample inside every timed step (SURVEY NEXT-2; implies --harness procs)")
     ap.add_argument("--graph-indptr", default="host",
                     help="with --sample gpu: 'host' or 'hbm' for indptr, optionally ',indices=hbm'")
     ap.add_argument("--async-sample", action="store_true",
@@ -1007,10 +1436,16 @@ def main(argv=None):
     ap.add_argument("--reverse-fanouts", action="store_true",
                     help="graphsage configs: apply the fanouts in reverse hop order (SURVEY c15)")
     ap.add_argument("--allreduce-smoke", action="store_true",
-                    help="N > 1: one untimed NCCL all-reduce of a 4-MB fp32 buffer after timing")
+                    help="procs harness, N > 1: one untimed NCCL all-reduce after timing")
+    ap.add_argument("--no-allreduce-smoke", action="store_true",
+                    help="threads harness: skip the untimed NCCL all-reduce smoke at N > 1")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if args.coop != "off" or args.sample != "cpu" or args.presort:
+        args.harness = "procs"
     spec = workload_spec(args.config)
     if args.reverse_fanouts and spec["kind"] == "graphsage":
         spec["reverse_fanouts"] = True          # DGL's order: the last fanout at the seeds (c15)
@@ -1018,14 +1453,30 @@ def main(argv=None):
     if args.graph_edges and spec["kind"] == "graphsage":
         spec["edges"] = args.graph_edges        # E sensitivity (reading c17)
     dist = Dist()
+    if dist.world > 1 and dist.world != args.gpus:
+        raise SystemExit(f"launched with WORLD_SIZE={dist.world} but --gpus {args.gpus}")
+    if dist.world == 1 and args.gpus > 1 and args.harness == "procs" and args.impl == "ut":
+        return self_launch(args, argv)
     try:
         if args.impl == "reference":
             run_reference(args, spec, dist)
+        elif args.harness == "procs":
+            run_procs(args, spec, dist)
+        elif dist.world > 1:
+            # launched by torchrun (one rank per GPU): rank 0 is the box process and drives every
+            # GPU over the one table; the other ranks only rendezvous (CPU gloo, no CUDA context)
+            dist.init("gloo")
+            if dist.rank == 0:
+                run_box(args, spec, dist)
+            elif args.dry_run:
+                dist.allreduce([1.0], "sum")
+            dist.barrier()
         else:
-            run_ut(args, spec, dist)
+            run_box(args, spec)
     finally:
         dist.close()
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -95,7 +95,10 @@ UT_API ut_table* ut_register(const void* host_ptr, uint64_t rows, uint64_t row_b
  *   UT_ALLOC_VMM_HOST  cuMemCreate(location HOST_NUMA of the current device) in 2-MiB granules,
  *                      mapped read/write for the device and the host.
  * *host_out receives the host (= device, UVA) address of the rows * row_bytes bytes; the memory
- * is owned by the table and freed by ut_release. Returns NULL on failure (UT_EINVAL /
+ * is owned by the table and freed by ut_release. The handle serves every device of the process
+ * (one table per box, one host thread per GPU): the first call on another device extends the
+ * mapping to it — SetAccessedBy(that device) for MANAGED, cuMemSetAccess for VMM_HOST (UT_ENOTSUP
+ * if the driver refuses); PINNED memory is Portable already. Returns NULL on failure (UT_EINVAL /
  * UT_ENOMEM / UT_ECUDA / UT_ENOTSUP via ut_last_error).
  */
 typedef enum ut_alloc_kind {
@@ -197,7 +200,8 @@ UT_API const char* ut_plan_probe(uint64_t base, uint64_t rows, uint64_t row_byte
  * "share=on|off|auto": neighbour line sharing for 16-B aligned tables with 128 < rb <= 512 —
  * the warp of a selected row also fetches its selected successor's bytes in the 128-B line the
  * two share, so the line is requested once; auto = on for gathers of >= 64K rows
- * that select >= 1/16 of the table. Costs rows x 4 B of stream-ordered scratch per gather.
+ * that select >= 1/16 of the table (host-known row counts only). Costs a hash of the selection,
+ * 8 B x 2^ceil(log2 2n), of stream-ordered scratch per gather (O(n), independent of the table).
  * "stage=on|off|auto" (auto = off): ut_gather_host's direct path gathers tiles of consecutive
  * output rows into shared memory and writes each tile's span with whole-line stores (k_staged;
  * an A/B knob — measured no gain).
@@ -260,6 +264,12 @@ UT_API int ut_graph_set_option(ut_graph* g, const char* option);
  * Synchronises `stream` once, at the end, to return the count (the sampler itself keeps every
  * size in device memory). Returns UT_OK, UT_EINVAL, UT_ERANGE (a seed outside [0, n_nodes); such
  * seeds are dropped), UT_ENOMEM or UT_ECUDA.
+ * Concurrency: ONE sample in flight per graph per device. The sampler's device state (frontier
+ * marks, dedup table, round counter) is per graph and device, so calls on one graph must be
+ * ordered on the device — issue them on one stream, or make the next call's stream wait for the
+ * previous one (this includes overlapping replays of a captured ut_sample_async). Different
+ * graphs, or different devices, are independent. (Unlike ut_gather, which is read-only on its
+ * table and safe from any number of streams.)
  */
 UT_API int ut_sample(ut_graph* g, const int64_t* seeds_dev, uint64_t n_seeds, const int32_t* fanouts,
                      int n_hops, uint64_t seed, int64_t* nodes_dev, uint64_t cap, uint64_t* n_out,

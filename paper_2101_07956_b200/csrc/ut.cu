@@ -42,67 +42,110 @@ int cuda_err(cudaError_t e, const char* what) {
   return set_err(UT_ECUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
 }
 
+// Page-locked and mapped for the GPU (cudaHostAlloc / cudaHostRegister / adopted)? When it is,
+// *end receives the end of the allocation range containing `a` if the driver reports it, else 0.
+static bool pinned_at(uint64_t a, uint64_t* end) {
+  cudaPointerAttributes at{};
+  const bool ok = cudaPointerGetAttributes(&at, (const void*)a) == cudaSuccess &&
+                  at.type == cudaMemoryTypeHost && at.devicePointer != nullptr;
+  cudaGetLastError();
+  *end = 0;
+  if (!ok) return false;
+  using PAttr = CUresult (*)(void*, CUpointer_attribute, CUdeviceptr);
+  static const PAttr attr_f = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuPointerGetAttribute", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PAttr) nullptr;
+    return reinterpret_cast<PAttr>(fn);
+  }();
+  CUdeviceptr start = 0;
+  size_t size = 0;
+  if (attr_f && attr_f(&start, CU_POINTER_ATTRIBUTE_RANGE_START_ADDR, (CUdeviceptr)a) == CUDA_SUCCESS &&
+      attr_f(&size, CU_POINTER_ATTRIBUTE_RANGE_SIZE, (CUdeviceptr)a) == CUDA_SUCCESS && size > 0 &&
+      (uint64_t)start <= a && a < (uint64_t)start + size)
+    *end = (uint64_t)start + size;
+  return true;
+}
+
+// Make [p, p+bytes) GPU-addressable in place. The common case registers the page-aligned range
+// in one call. If part of it is already page-locked (cudaHostAlloc'd by the caller, or pages a
+// neighbouring registration holds), the range is walked allocation by allocation: pinned
+// stretches are adopted (their extent from the driver's range attributes, else page by page)
+// and every unpinned gap is registered, splitting a gap in halves where the driver refuses it
+// because a pinned island lies inside. Every byte is covered before the table is used.
 int pin_host(const void* p, uint64_t bytes, bool read_only, Pin* out) {
   *out = Pin{};
-  cudaPointerAttributes attr{}, attr_end{};
-  cudaError_t e = cudaPointerGetAttributes(&attr, p);
-  cudaError_t e2 = cudaPointerGetAttributes(&attr_end, (const uint8_t*)p + bytes - 1);
-  if (e == cudaSuccess && e2 == cudaSuccess && attr.type == cudaMemoryTypeHost &&
-      attr_end.type == cudaMemoryTypeHost && attr.devicePointer != nullptr) {
-    out->base = (const uint8_t*)p;
-    out->len = bytes;
-    return UT_OK;
-  }
-  cudaGetLastError();
   int dev = 0, ro_ok = 0;
   cudaGetDevice(&dev);
   if (read_only) cudaDeviceGetAttribute(&ro_ok, cudaDevAttrHostRegisterReadOnlySupported, dev);
   const uint64_t pg = (uint64_t)sysconf(_SC_PAGESIZE);
   const uint64_t lo = (uint64_t)p / pg * pg;
   const uint64_t hi = ((uint64_t)p + bytes + pg - 1) / pg * pg;
-  unsigned flags = cudaHostRegisterPortable | cudaHostRegisterMapped;
-  e = cudaErrorUnknown;
-  if (ro_ok) {
-    e = cudaHostRegister((void*)lo, hi - lo, flags | cudaHostRegisterReadOnly);
-    if (e == cudaSuccess) out->read_only = 1;
-    else cudaGetLastError();
-  }
-  if (e != cudaSuccess) e = cudaHostRegister((void*)lo, hi - lo, flags);
-  uint64_t rlo = lo, rhi = hi;
-  if (e == cudaErrorHostMemoryAlreadyRegistered) {
-    // a neighbouring allocation registered the first and/or last page: pin the rest
-    cudaGetLastError();
-    auto pinned = [](uint64_t a) {
-      cudaPointerAttributes at{};
-      bool ok = cudaPointerGetAttributes(&at, (const void*)a) == cudaSuccess &&
-                at.type == cudaMemoryTypeHost;
-      cudaGetLastError();
-      return ok;
-    };
-    if (pinned(rlo)) rlo += pg;
-    if (rhi > rlo && pinned(rhi - 1)) rhi -= pg;
-    if (rlo >= rhi) {
-      out->base = (const uint8_t*)p;   // every page is already pinned by someone else
-      out->len = bytes;
-      return UT_OK;
+  const unsigned flags = cudaHostRegisterPortable | cudaHostRegisterMapped;
+  int ro_all = 1;
+  auto reg = [&](uint64_t a, uint64_t len) -> cudaError_t {
+    cudaError_t e = cudaErrorUnknown;
+    if (ro_ok) {
+      e = cudaHostRegister((void*)a, len, flags | cudaHostRegisterReadOnly);
+      if (e != cudaSuccess) cudaGetLastError();
     }
-    e = cudaHostRegister((void*)rlo, rhi - rlo, flags);
-  }
-  if (e != cudaSuccess) {
-    cudaGetLastError();
+    if (e != cudaSuccess) {
+      e = cudaHostRegister((void*)a, len, flags);
+      if (e != cudaSuccess) cudaGetLastError();
+      else ro_all = 0;
+    }
+    if (e == cudaSuccess) out->regs.emplace_back((const uint8_t*)a, len);
+    return e;
+  };
+  auto fail = [&](cudaError_t e, uint64_t len) {
+    unpin_host(out);
     if (e == cudaErrorMemoryAllocation)
-      return set_err(UT_ENOMEM, "cudaHostRegister(%llu bytes): %s", (unsigned long long)(hi - lo),
+      return set_err(UT_ENOMEM, "cudaHostRegister(%llu bytes): %s", (unsigned long long)len,
                      cudaGetErrorString(e));
     return cuda_err(e, "cudaHostRegister");
+  };
+  uint64_t end0 = 0, end1 = 0;
+  if (pinned_at((uint64_t)p, &end0) && end0 >= (uint64_t)p + bytes) {
+    out->base = (const uint8_t*)lo;   // one pinned allocation holds every byte: adopt it
+    out->len = hi - lo;
+    return UT_OK;
   }
-  out->base = (const uint8_t*)rlo;
-  out->len = rhi - rlo;
-  out->registered = 1;
+  cudaError_t e = reg(lo, hi - lo);
+  if (e != cudaSuccess && e != cudaErrorHostMemoryAlreadyRegistered &&
+      (pinned_at(lo, &end0) || pinned_at(hi - 1, &end1)))
+    e = cudaErrorHostMemoryAlreadyRegistered;   // some driver paths report overlap differently
+  if (e != cudaSuccess && e != cudaErrorHostMemoryAlreadyRegistered) return fail(e, hi - lo);
+  if (e != cudaSuccess) {
+    ro_all = 0;                     // adopted stretches keep their owner's flags
+    uint64_t a = lo;
+    while (a < hi) {
+      uint64_t end = 0;
+      if (pinned_at(a, &end)) {     // adopt this allocation's stretch
+        a = end > a ? std::min(hi, (end + pg - 1) / pg * pg) : a + pg;
+        continue;
+      }
+      // an unpinned gap starting at a: register [a, hi), halving on refusal
+      uint64_t len = hi - a;
+      for (;;) {
+        e = reg(a, len);
+        if (e == cudaSuccess) break;
+        if (e == cudaErrorMemoryAllocation || len <= pg) return fail(e, len);
+        len = (len / 2 + pg - 1) / pg * pg;
+      }
+      a += len;
+    }
+  }
+  out->base = (const uint8_t*)lo;
+  out->len = hi - lo;
+  out->read_only = ro_all;
   return UT_OK;
 }
 
 void unpin_host(Pin* pin) {
-  if (pin->registered) cudaHostUnregister(const_cast<uint8_t*>(pin->base));
+  for (auto& r : pin->regs) cudaHostUnregister(const_cast<uint8_t*>(r.first));
+  cudaGetLastError();
   *pin = Pin{};
 }
 
@@ -114,10 +157,13 @@ int pin_device_ptr(const Pin& pin, const void* p, uint64_t* dev) {
     *dev = (uint64_t)p;
     return UT_OK;
   }
+  // without UVA the device addresses of separate registrations are not contiguous
+  if (pin.regs.size() != 1 || pin.regs[0].first != pin.base || pin.regs[0].second != pin.len)
+    return set_err(UT_ENOTSUP, "table is not one registration and the device has no UVA");
   void* dp = nullptr;
-  cudaError_t e = cudaHostGetDevicePointer(&dp, const_cast<uint8_t*>(pin.base), 0);
+  cudaError_t e = cudaHostGetDevicePointer(&dp, const_cast<void*>(p), 0);
   if (e != cudaSuccess) return cuda_err(e, "cudaHostGetDevicePointer");
-  *dev = (uint64_t)dp + ((uint64_t)p - (uint64_t)pin.base);
+  *dev = (uint64_t)dp;
   return UT_OK;
 }
 
@@ -265,8 +311,10 @@ struct DevState {
   cudaEvent_t drained[kBuf] = {};
   int64_t* idx_all = nullptr;           // ut_gather_host zero-copy path: device copy of idx
   uint64_t idx_cap = 0;
+  std::mutex hmu;                       // ut_gather_host: this device's host-form scratch
   CUtensorMap tmap;                     // "tma4" plan: the table as a rows x (rb/4) word tensor
-  bool tmap_ok = false;
+  std::mutex tmap_mu;                   // builds tmap once (never t->mu: ut_gather_host's
+  std::atomic<bool> tmap_ok{false};     // caller may hold other locks)
 };
 
 }  // namespace
@@ -274,8 +322,7 @@ struct DevState {
 struct ut_table {
   const uint8_t* host = nullptr;
   uint64_t rows = 0, rb = 0, bytes = 0;
-  const uint8_t* reg_base = nullptr;   // page-aligned registered range
-  uint64_t reg_len = 0;
+  Pin pin;                              // ut_register: pages pinned or adopted in place
   int registered = 0, read_only = 0, device = 0;
   int alloc_kind = -1;                  // ut_create: ut_alloc_kind; -1 = caller memory
   bool direct_va = false;               // device address == host address (managed / VMM)
@@ -294,6 +341,39 @@ struct ut_table {
 
 namespace {
 
+// The paper's advice for a unified tensor (Table 2) on one more device: the
+// pages stay in host memory (SetPreferredLocation = CPU, set at creation) and `dev` maps them.
+int managed_accessed_by(const void* p, uint64_t bytes, int dev) {
+  cudaMemLocation gpu{};
+  gpu.type = cudaMemLocationTypeDevice;
+  gpu.id = dev;
+  cudaError_t e = cudaMemAdvise(p, bytes, cudaMemAdviseSetAccessedBy, gpu);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return cuda_err(e, "cudaMemAdvise(SetAccessedBy)");
+  }
+  return UT_OK;
+}
+
+// Map a VMM host allocation (cuMemCreate HOST_NUMA) for one more device.
+int vmm_grant(const void* va, uint64_t size, int dev) {
+  using PAccess = CUresult (*)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  if (cudaGetDriverEntryPoint("cuMemSetAccess", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return set_err(UT_ENOTSUP, "cuMemSetAccess unavailable");
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = dev;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  CUresult r = reinterpret_cast<PAccess>(fn)((CUdeviceptr)va, size, &acc, 1);
+  if (r != CUDA_SUCCESS)
+    return set_err(UT_ENOTSUP, "cuMemSetAccess(device %d) failed (%d): this VMM host table "
+                   "cannot be mapped on that device", dev, (int)r);
+  return UT_OK;
+}
+
 // Lazily resolve the table's device address and error word on the current device.
 int dev_state(const ut_table* ct, DevState** out) {
   ut_table* t = const_cast<ut_table*>(ct);
@@ -310,10 +390,15 @@ int dev_state(const ut_table* ct, DevState** out) {
   if (!s->init) {
     uint64_t dev_base = (uint64_t)t->host;
     if (!t->direct_va) {
-      Pin pin;
-      pin.base = t->reg_base;
-      pin.len = t->reg_len;
-      if (pin_device_ptr(pin, t->host, &dev_base) != UT_OK) return UT_ECUDA;
+      if (pin_device_ptr(t->pin, t->host, &dev_base) != UT_OK) return UT_ECUDA;
+    }
+    if (dev != t->device) {
+      // a library-owned table used from another device of the process (one table per box,
+      // one thread per GPU): extend the creator's mapping to this device
+      int rc = UT_OK;
+      if (t->alloc_kind == UT_ALLOC_MANAGED) rc = managed_accessed_by(t->host, t->bytes, dev);
+      else if (t->alloc_kind == UT_ALLOC_VMM_HOST) rc = vmm_grant(t->host, t->vmm_bytes, dev);
+      if (rc != UT_OK) return rc;
     }
     unsigned long long* err = nullptr;
     e = cudaMalloc(&err, sizeof *err);
@@ -577,15 +662,15 @@ cudaError_t launch_staged(const ut_table* t, DevState* s, cudaStream_t st, const
 }
 
 int gather_runs(const ut_table* t, DevState* s, const Plan& p, const ut::GatherArgs& a, cudaStream_t st);
-bool want_share(const ut_table* t, const Plan& p, uint64_t n);
+bool want_share(const ut_table* t, const Plan& p, uint64_t n, bool dev_n);
 int gather_share(const ut_table* t, DevState* s, const ut::GatherArgs& a, cudaStream_t st);
 
 // The table as a 2-D tensor of rows x (rb/4) 32-bit words for the "tma4" plan (built once per
 // device; cuTensorMapEncodeTiled through the runtime's driver entry point).
-int tensor_map(const ut_table* ct, DevState* s) {
-  ut_table* t = const_cast<ut_table*>(ct);
-  std::lock_guard<std::mutex> lk(t->mu);
-  if (s->tmap_ok) return UT_OK;
+int tensor_map(const ut_table* t, DevState* s) {
+  if (s->tmap_ok.load(std::memory_order_acquire)) return UT_OK;
+  std::lock_guard<std::mutex> lk(s->tmap_mu);
+  if (s->tmap_ok.load(std::memory_order_relaxed)) return UT_OK;
   typedef CUresult (*PEncode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -603,7 +688,7 @@ int tensor_map(const ut_table* ct, DevState* s) {
                                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_err(UT_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  s->tmap_ok = true;
+  s->tmap_ok.store(true, std::memory_order_release);
   return UT_OK;
 }
 
@@ -622,7 +707,7 @@ int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n
   cudaError_t e;
   s->rows += n;
   s->bytes += n * t->rb;
-  if (want_share(t, p, n)) {
+  if (want_share(t, p, n, n_dev != nullptr)) {
     const int rc = gather_share(t, s, a, st);
     if (rc != UT_ENOMEM) return rc;          // no room for the slot array: the plain gather below
   }
@@ -812,48 +897,51 @@ int gather_runs(const ut_table* t, DevState* s, const Plan& p, const ut::GatherA
 
 // Neighbour line sharing: vec16 tables with 128 < rb <= 512 whose row boundaries
 // are not all on 128-B lines. "auto" takes it for gathers of >= 64K rows that select >= 1/16 of
-// the table (so that a selected row's successor is selected often enough to pay for the
-// rows x 4 B slot array), with the slot array <= 1 GiB.
-bool want_share(const ut_table* t, const Plan& p, uint64_t n) {
+// the table (so that a selected row's successor is selected often enough to pay for the hash of
+// the selection), with the row count known on the host (a device-count gather's max_n is only a
+// bound).
+bool want_share(const ut_table* t, const Plan& p, uint64_t n, bool dev_n) {
   if (t->share == 0 || p.kind != P_VEC16 || t->rb <= 128 || t->rb > 512) return false;
   if ((((uint64_t)t->host | t->rb) & 127) == 0) return false;     // no partial lines to share
-  if (n == 0 || n >= (1ull << 31) || t->rows > (1ull << 28)) return false;
+  if (n == 0 || n >= (1ull << 31) || t->rows >= 0xFFFFFFFFull) return false;
   if (t->share == 1) return true;
-  if (t->reorder == 1 || t->runs == 1) return false;
+  if (t->reorder == 1 || t->runs == 1 || dev_n) return false;
   return n >= 65536 && n * 16 >= t->rows;
 }
 
+// Scratch: the selection hash, 8 B x 2^bits with 2^bits >= 2n (O(n), not O(rows)), stream-ordered
+// from the library's pool. The clear, the mark and the gather are all inside timed(), so
+// gather_kernel_ms (and bench's roofline.achieved) carry the whole cost of sharing.
 int gather_share(const ut_table* t, DevState* s, const ut::GatherArgs& a, cudaStream_t st) {
-  uint32_t* slot = nullptr;
+  uint32_t bits = 1;
+  while ((1ull << bits) < 2 * a.n) ++bits;
+  const size_t bytes = (size_t)8 << bits;
+  ut::ShareHash hs{nullptr, bits};
   cudaError_t e;
-  if ((e = cudaMallocFromPoolAsync((void**)&slot, t->rows * sizeof(uint32_t), s->pool, st)) != cudaSuccess) {
+  if ((e = cudaMallocFromPoolAsync((void**)&hs.slots, bytes, s->pool, st)) != cudaSuccess) {
     cudaGetLastError();
     return UT_ENOMEM;
   }
-  e = cudaMemsetAsync(slot, 0, t->rows * sizeof(uint32_t), st);
-  if (e == cudaSuccess) {
+  e = timed(t, s, st, [&] {
+    cudaError_t e1 = cudaMemsetAsync(hs.slots, 0, bytes, st);
+    if (e1 != cudaSuccess) return e1;
     const int gm = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)s->sms * 8, (a.n + 255) / 256));
-    ut::k_share_mark<<<gm, 256, 0, st>>>(a, slot);
+    ut::k_share_mark<<<gm, 256, 0, st>>>(a, hs);
     s->launches += 1;
     s->shared += 1;
-    e = cudaGetLastError();
-  }
-  if (e == cudaSuccess) {
-    e = timed(t, s, st, [&] {
-      const uint64_t tiles = (a.n + kU - 1) / kU;
-      if (t->rb > 400) {
-        auto k = ut::k_share<kU, true>;
-        k<<<grid_for(k, s->sms, tiles, -2), 256, 0, st>>>(a, slot);
-      } else {
-        auto k = ut::k_share<kU, false>;
-        k<<<grid_for(k, s->sms, tiles, -2), 256, 0, st>>>(a, slot);
-      }
-      return cudaGetLastError();
-    });
-  }
-  cudaError_t e2 = cudaFreeAsync(slot, st);
+    const uint64_t tiles = (a.n + kU - 1) / kU;
+    if (t->rb > 400) {
+      auto k = ut::k_share<kU, true>;
+      k<<<grid_for(k, s->sms, tiles, -2), 256, 0, st>>>(a, hs);
+    } else {
+      auto k = ut::k_share<kU, false>;
+      k<<<grid_for(k, s->sms, tiles, -2), 256, 0, st>>>(a, hs);
+    }
+    return cudaGetLastError();
+  });
+  cudaError_t e2 = cudaFreeAsync(hs.slots, st);
   if (e != cudaSuccess) return cuda_err(e, "shared-line gather");
-  if (e2 != cudaSuccess) return cuda_err(e2, "cudaFreeAsync(share slots)");
+  if (e2 != cudaSuccess) return cuda_err(e2, "cudaFreeAsync(share hash)");
   return UT_OK;
 }
 
@@ -901,15 +989,12 @@ ut_table* ut_register(const void* host_ptr, uint64_t rows, uint64_t row_bytes) {
 
   // Already page-locked and mapped (cudaHostAlloc / a previous registration)? Adopt it;
   // otherwise pin the page-aligned range in place.
-  Pin pin;
-  if (pin_host(host_ptr, bytes, true, &pin) != UT_OK) {
+  if (pin_host(host_ptr, bytes, true, &t->pin) != UT_OK) {
     delete t;
     return nullptr;
   }
-  t->reg_base = pin.base;
-  t->reg_len = pin.len;
-  t->registered = pin.registered;
-  t->read_only = pin.read_only;
+  t->registered = t->pin.registered();
+  t->read_only = t->pin.read_only;
   const char* env = getenv("UT_PLAN");
   if (env && *env) {
     bool ok;
@@ -1077,8 +1162,6 @@ ut_table* ut_create(const void* src, uint64_t rows, uint64_t row_bytes, int kind
   t->rb = row_bytes;
   t->bytes = bytes;
   t->device = dev;
-  t->reg_base = (const uint8_t*)p;
-  t->reg_len = bytes;
   t->alloc_kind = kind;
   t->direct_va = kind != UT_ALLOC_PINNED;
   t->vmm_handle = vmm_h;
@@ -1131,7 +1214,8 @@ int ut_gather_host(const ut_table* ct, const int64_t* idx_host, uint64_t n, void
   DevState* s;
   int rc = dev_state(t, &s);
   if (rc != UT_OK) return rc;
-  std::lock_guard<std::mutex> lk(t->mu);
+  // per-device lock of the host-form scratch only: gathers on other devices run concurrently
+  std::lock_guard<std::mutex> lk(s->hmu);
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e;
   // Fast path: out_host is page-locked and mapped, so the gather kernel stores the rows straight
@@ -1251,8 +1335,8 @@ int ut_release(ut_table* t) {
     }
   }
   cudaSetDevice(cur);
-  if (t->registered) {
-    cudaError_t e = cudaHostUnregister(const_cast<uint8_t*>(t->reg_base));
+  for (auto& r : t->pin.regs) {
+    cudaError_t e = cudaHostUnregister(const_cast<uint8_t*>(r.first));
     if (e != cudaSuccess) rc = cuda_err(e, "cudaHostUnregister");
   }
   if (t->alloc_kind == UT_ALLOC_PINNED) cudaFreeHost(const_cast<uint8_t*>(t->host));

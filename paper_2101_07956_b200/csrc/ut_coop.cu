@@ -544,8 +544,15 @@ int ut_coop_gather(ut_coop* c, const int64_t* idx_dev, uint64_t n, void* out_dev
   if (bad != UT_OK) n = 0;
   int rc = ut_coop_dispatch(c, idx_dev, n, stream);
   if (rc == UT_OK && c->world > 1) rc = device_barrier(c, 0, (cudaStream_t)stream);
-  if (rc == UT_OK) rc = ut_coop_fetch(c, stream);
-  if (rc == UT_OK && c->world > 1) rc = device_barrier(c, 1, (cudaStream_t)stream);
+  if (rc == UT_OK) {
+    // once barrier 0 is enqueued the peers' streams wait for this rank's barrier-1 flags: write
+    // them even when the fetch fails (its error is reported after), or the peers hang
+    const int frc = ut_coop_fetch(c, stream);
+    char fmsg[512] = "";
+    if (frc != UT_OK) ut_last_error(fmsg, sizeof fmsg);
+    if (c->world > 1) rc = device_barrier(c, 1, (cudaStream_t)stream);
+    if (frc != UT_OK) return set_err(frc, "%s", fmsg);
+  }
   if (rc == UT_OK) rc = ut_coop_combine(c, out_dev, stream);
   if (rc == UT_OK && bad != UT_OK) {
     char msg[512];

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <utility>
+#include <vector>
 
 namespace utx {
 
@@ -13,10 +15,12 @@ int cuda_err(cudaError_t e, const char* what);
 // Host memory made GPU-addressable in place: adopted when already page-locked and mapped,
 // otherwise cudaHostRegister(Portable|Mapped[|ReadOnly]) of the page-aligned range.
 struct Pin {
-  const uint8_t* base = nullptr;   // registered (page-aligned) range, or the adopted pointer
+  const uint8_t* base = nullptr;   // page-aligned range covering the caller's bytes
   uint64_t len = 0;
-  int registered = 0;              // 1: unpin_host unregisters
-  int read_only = 0;
+  std::vector<std::pair<const uint8_t*, uint64_t>> regs;   // what we registered (unpin_host
+                                                           // unregisters); the rest is adopted
+  int read_only = 0;               // 1: every page registered here with cudaHostRegisterReadOnly
+  int registered() const { return regs.empty() ? 0 : 1; }
 };
 int pin_host(const void* p, uint64_t bytes, bool read_only, Pin* out);
 void unpin_host(Pin* pin);

@@ -834,19 +834,44 @@ __global__ void __launch_bounds__(256) k_runs(GatherArgs a_, const uint32_t* __r
 // Neighbour line sharing ("share", vec16 tables with 128 < rb <= 512). Selected
 // rows r and r+1 whose boundary does not fall on a 128-B line both touch that line; fetched by
 // both warps it costs two sysmem requests, and at these widths the request count, not the bytes,
-// bounds the link. k_share_mark gives every selected row one canonical work item,
-// slot[r] = i + 1 (0 = not selected; any one occurrence of a duplicated row wins). In k_share
-// the warp of row r also loads the bytes of row r+1 that lie in r's last line and stores them
-// into row r+1's canonical output row; that canonical item skips its first (shared) line. Both
-// sides decide from the same slot[] — fixed for the whole gather — so every output byte is
-// written by its own row's warp or by a predecessor's warp that read the same table bytes
-// (duplicates of r write identical bytes). The result is the plain gather (oracle), unchanged.
-__global__ void __launch_bounds__(256) k_share_mark(GatherArgs a_, uint32_t* __restrict__ slot) {
+// bounds the link. k_share_mark gives every selected row one canonical work item
+// (any one occurrence of a duplicated row wins) in a per-gather hash of the selection, O(n):
+// 2^bits >= 2n slots of one 64-bit word, (r + 1) << 32 | (i + 1), open addressing with linear
+// probing, 0 = empty. In k_share the warp of row r also loads the bytes of row r+1 that lie in r's
+// last line and stores them into row r+1's canonical output row; that canonical item skips its
+// first (shared) line. Both sides decide from the same table — fixed for the whole gather — so
+// every output byte is written by its own row's warp or by a predecessor's warp that read the
+// same table bytes (duplicates of r write identical bytes). The result is the plain gather
+// (oracle), unchanged.
+struct ShareHash {
+  unsigned long long* slots;
+  uint32_t bits;
+  __device__ __forceinline__ uint64_t home(uint64_t r) const {
+    return (r * 0x9E3779B97F4A7C15ull) >> (64 - bits);
+  }
+  // canonical work item + 1 of row r, 0 when r is not selected
+  __device__ __forceinline__ uint32_t find(uint64_t r) const {
+    const uint64_t mask = (1ull << bits) - 1, key = r + 1;
+    for (uint64_t h = home(r);; h = (h + 1) & mask) {
+      const unsigned long long w = __ldcg(slots + h);
+      if (w == 0ull) return 0u;
+      if ((w >> 32) == key) return (uint32_t)w;
+    }
+  }
+};
+
+__global__ void __launch_bounds__(256) k_share_mark(GatherArgs a_, ShareHash hs) {
   const GatherArgs a = with_dev_n(a_);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t mask = (1ull << hs.bits) - 1;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
     const int64_t r = __ldg(a.idx + i);
-    if ((uint64_t)r < a.rows) slot[r] = (uint32_t)(i + 1);
+    if ((uint64_t)r >= a.rows) continue;
+    const unsigned long long w = ((unsigned long long)(r + 1) << 32) | (uint32_t)(i + 1);
+    for (uint64_t h = hs.home((uint64_t)r);; h = (h + 1) & mask) {
+      const unsigned long long old = atomicCAS(hs.slots + h, 0ull, w);
+      if (old == 0ull || (old >> 32) == (unsigned long long)(r + 1)) break;
+    }
   }
 }
 
@@ -854,7 +879,7 @@ __global__ void __launch_bounds__(256) k_share_mark(GatherArgs a_, uint32_t* __r
 // TWO, rows > 400 B) of the byte range [lo, hi) relative to the row start: lo skips the shared
 // first line, hi extends over the successor's bytes in the last line.
 template <int U, bool TWO>
-__global__ void __launch_bounds__(256, UT_MINB) k_share(GatherArgs a_, const uint32_t* __restrict__ slot) {
+__global__ void __launch_bounds__(256, UT_MINB) k_share(GatherArgs a_, ShareHash hs) {
   const GatherArgs a = with_dev_n(a_);
   constexpr int C = TWO ? 2 : 1;
   const int lane = threadIdx.x & 31;
@@ -877,11 +902,11 @@ __global__ void __launch_bounds__(256, UT_MINB) k_share(GatherArgs a_, const uin
       hi[u] = (uint32_t)a.rb;
       nxt[u] = 0;
       if (ok[u]) {
-        if ((s & 127) && r > 0 && __ldg(slot + r) == (uint32_t)(i + 1) && __ldg(slot + r - 1) != 0u)
+        if ((s & 127) && r > 0 && hs.find((uint64_t)r) == (uint32_t)(i + 1) && hs.find((uint64_t)r - 1) != 0u)
           lo[u] = 128u - (uint32_t)(s & 127);
         const uint64_t e = s + a.rb;
         if ((e & 127) && (uint64_t)r + 1 < a.rows) {
-          const uint32_t nx = __ldg(slot + r + 1);
+          const uint32_t nx = hs.find((uint64_t)r + 1);
           if (nx) {
             hi[u] = (uint32_t)a.rb + 128u - (uint32_t)(e & 127);
             nxt[u] = nx;
