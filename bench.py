@@ -500,10 +500,14 @@ def run_procs(args, spec, dist):
         for k in range(n_check):
             l = lists[k]
             if partitioned:
-                # no process holds the whole table: the expected rows are the table's definition
-                # (the input generator's row content), every id here is in range
-                workloads.fill_rows(want_buf, l, rb, seed)
-                bad = -1
+                # no process holds the whole table: build the sub-table of this list's distinct
+                # rows (input generation: the table content of those ids, ascending) and let the
+                # oracle gather from it with the ids remapped to sub-table rows
+                uniq = np.unique(l)
+                sub = np.empty(uniq.size * rb, dtype=np.uint8)
+                workloads.fill_rows(sub, uniq, rb, seed)
+                bad = oracle.gather_into(sub.ctypes.data, uniq.size, rb,
+                                         np.searchsorted(uniq, l).astype(np.int64), want_buf)
             else:
                 bad = oracle.gather_into(hb.addr, spec["rows"], rb, l, want_buf)
             gather(idx_dev[k], out[: l.size * rb])

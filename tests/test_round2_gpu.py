@@ -120,7 +120,9 @@ def test_share_hash_sparse_selection_of_large_table():
             t.gather(torch.from_numpy(idx).cuda(), out=buf[off:])
             assert buf[off:].cpu().numpy().tobytes() == want.tobytes()
             assert t.error_pos() == bad
-        assert t.stats()["share_gathers"] == 2
+        # the 16-B aligned output takes the shared-line kernel; the misaligned one (off 4) has
+        # no vec16 plan and so realigns without sharing
+        assert t.stats()["share_gathers"] == 1
     hb.close()
 
 

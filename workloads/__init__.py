@@ -92,7 +92,8 @@ def fill_table(dst, rows: int, rb: int, seed: int, threads: int = 0) -> None:
 
 
 def fill_rows(dst, ids: np.ndarray, rb: int, seed: int, threads: int = 0) -> None:
-    """Row k of ``dst`` = the content fill_table gives row ids[k] (zero row for ids[k] < 0)."""
+    """Row k of ``dst`` = the content fill_table gives row ids[k] (zero row for ids[k] < 0): a
+    partition or sub-table of chosen rows — table input, never an expected gather result."""
     ids = np.ascontiguousarray(ids, dtype=np.int64)
     if isinstance(dst, np.ndarray):
         assert dst.nbytes >= ids.size * rb

@@ -2,8 +2,10 @@
  * workloads/gen.c — seeded synthetic INPUT generators (no gather arithmetic).
  *
  * Shared by the tests, the oracle side and the CUDA side as the source of inputs only: it
- * fills the host feature table and draws uniform index lists. It computes nothing the gather
- * computes (no row addressing of an index list, no copying of rows by index).
+ * fills the host feature table (whole, or the sub-table of chosen row ids, gen_fill_rows) and
+ * draws uniform index lists. It copies no rows: every row it writes is computed from its id and
+ * the seed, the table's definition. It is never the source of an expected gather result — those
+ * come from oracle/ only (bench builds a sub-table here and gathers from it with the oracle).
  *
  * Recipe:
  *   splitmix64(x): the standard SplitMix64 finaliser.
@@ -55,7 +57,8 @@ void gen_fill_table(uint8_t* dst, uint64_t rows, uint64_t rb, uint64_t seed, int
 }
 
 /* Row k of dst = the self-identifying content of table row ids[k] (as gen_fill_table writes it);
- * ids[k] < 0 gives a zero row. Fills a partition of a table, or the expected rows of a gather. */
+ * ids[k] < 0 gives a zero row. Fills a partition of a table or a sub-table of chosen rows
+ * (table input, not an expected gather result). */
 void gen_fill_rows(uint8_t* dst, const int64_t* ids, uint64_t n, uint64_t rb, uint64_t seed, int threads)
 {
     int nt = threads > 0 ? threads : omp_get_max_threads();
