@@ -275,12 +275,21 @@ def ncu_traffic(workload: str, plan: str, table_memory: str, args) -> dict:
     if (not rec or rec.get("plan") != plan or rec.get("table_memory", table_memory) != table_memory
             or args.plan or args.sample != "cpu" or args.coop != "off"):
         return {"traffic": None}
-    return {"traffic": rec["hbm_bytes_per_launch"],
-            "traffic_detail": {k: rec[k] for k in ("hbm_bytes_per_launch", "hbm_write_bytes_per_launch",
-                                                   "sysmem_bytes_per_launch", "sysmem_requests_per_launch",
-                                                   "pcie_read_bytes_per_launch",
-                                                   "algorithmic_bytes_per_launch", "launches",
-                                                   "source") if k in rec}}
+    detail = {k: rec[k] for k in ("hbm_bytes_per_launch", "hbm_write_bytes_per_launch",
+                                  "sysmem_bytes_per_launch", "sysmem_requests_per_launch",
+                                  "pcie_read_bytes_per_launch", "algorithmic_bytes_per_launch",
+                                  "launches", "source") if k in rec}
+    alg = rec.get("algorithmic_bytes_per_launch")
+    if alg and rec.get("pcie_read_bytes_per_launch") and rec.get("sysmem_bytes_per_launch"):
+        # link bytes per useful byte, split (calibrated by request_rate_probe):
+        # 32-B sector over-fetch, then a fixed per-request cost the PCIe counter adds
+        req = rec.get("sysmem_requests_per_launch") or 1
+        detail["pcie_read_over_algorithmic"] = round(rec["pcie_read_bytes_per_launch"] / alg, 4)
+        detail["sectors_over_algorithmic"] = round(rec["sysmem_bytes_per_launch"] / alg, 4)
+        detail["pcie_bytes_per_request_beyond_sectors"] = round(
+            (rec["pcie_read_bytes_per_launch"] - rec["sysmem_bytes_per_launch"]) / req, 2)
+        detail["payload_bytes_per_request"] = round(alg / req, 1)
+    return {"traffic": rec["hbm_bytes_per_launch"], "traffic_detail": detail}
 
 
 def cpu_oracle_rate(table_addr: int, spec: dict, lists: list[np.ndarray], budget_s: float):
@@ -935,6 +944,8 @@ def run_box(args, spec, dist=None):
     count = min(args.warmup + args.steps, args.max_lists)
     procs = max(1, (os.cpu_count() or 1) // max(1, min(N, 4)))
     lists = [make_index_lists(spec, g, N, count, seed, procs) for g in range(N)]  # before CUDA
+    if args.presort:   # experiment only: what a perfectly address-ordered list would give
+        lists = [[np.sort(l) for l in ls] for ls in lists]
     timed_lists = [lists[0][(args.warmup + s) % count] for s in range(args.steps)]
     if args.dry_run:
         rows, rb = spec["rows"], spec["row_bytes"]
@@ -964,8 +975,9 @@ def run_box(args, spec, dist=None):
 
     import torch
     ndev = torch.cuda.device_count()
-    if ndev < N:
+    if ndev < N and not args.oversubscribe:
         raise SystemExit(f"--gpus {N}: only {ndev} CUDA device(s) visible")
+    dev_of = (lambda g: g % ndev) if args.oversubscribe else (lambda g: g)
     torch.cuda.set_device(0)
     import paper_2101_07956_b200 as ut
     t_reg = time.perf_counter()
@@ -975,35 +987,45 @@ def run_box(args, spec, dist=None):
         for p in args.plan.split(","):
             table.set_plan(p)
     rb = spec["row_bytes"]
-    workers = run_threads(N, lambda g: BoxWorker(g, torch, table, spec, lists[g], args))
+    workers = run_threads(N, lambda g: BoxWorker(dev_of(g), torch, table, spec, lists[g], args))
 
     # roofline denominators, measured now: each GPU's link alone, then all at once
+    ndevs = len({dev_of(g) for g in range(N)})
+
     def link(g, reps=10):
-        torch.cuda.set_device(g)
+        torch.cuda.set_device(dev_of(g))
         return h2d_ceiling(torch, stream=workers[g].stream, reps=reps)
-    link_solo = [link(g) for g in range(N)]
-    link_conc = run_threads(N, link) if N > 1 else list(link_solo)
+    link_solo = [link(g) for g in range(ndevs)]
+    link_conc = run_threads(ndevs, link) if ndevs > 1 else list(link_solo)
     torch.cuda.set_device(0)
     sm_ceiling = sm_read_ceiling(torch, ut)
 
     parity_lists = 0
     if args.check:
         budget = (16 << 30) // N
-        parity_lists = sum(run_threads(N, lambda g: (torch.cuda.set_device(g),
+        parity_lists = sum(run_threads(N, lambda g: (torch.cuda.set_device(dev_of(g)),
                                                       workers[g].parity(hb.addr, budget))[1]))
 
-    clocks = ClockSampler(list(range(N)))
+    clocks = ClockSampler(sorted({dev_of(g) for g in range(N)}))
     clocks.start()
-    run_threads(N, lambda g: (torch.cuda.set_device(g), workers[g].warmup()))
+    run_threads(N, lambda g: (torch.cuda.set_device(dev_of(g)), workers[g].warmup()))
     table.set_plan("timing=on")
-    run_threads(N, lambda g: (torch.cuda.set_device(g), table.stats(reset=True)))
+    devices = sorted({dev_of(g) for g in range(N)})
+
+    def dev_stats():      # the library counts per device
+        out = []
+        for d in devices:
+            torch.cuda.set_device(d)
+            out.append(table.stats(reset=True))
+        return out
+    dev_stats()
     start = threading.Barrier(N)
-    res = run_threads(N, lambda g: (torch.cuda.set_device(g), workers[g].timed(start))[1])
+    res = run_threads(N, lambda g: (torch.cuda.set_device(dev_of(g)), workers[g].timed(start))[1])
     clk = clocks.stop()
-    stats = run_threads(N, lambda g: (torch.cuda.set_device(g), table.stats(reset=True))[1])
+    stats = dev_stats()
     table.set_plan("timing=off")
     # the link ceiling again, right after timing: box drift shows as a change here
-    link_after = run_threads(N, lambda g: link(g, reps=5)) if N > 1 else [link(0, reps=5)]
+    link_after = run_threads(ndevs, lambda g: link(g, reps=5)) if ndevs > 1 else [link(0, reps=5)]
 
     dev_ms = [sum(r["ms"]) for r in res]
     total = sum(r["bytes"] for r in res)
@@ -1011,7 +1033,8 @@ def run_box(args, spec, dist=None):
     per_gpu = [r["bytes"] / (m / 1e3) / 1e9 for r, m in zip(res, dev_ms)]
     kern_ms = sum(s["gather_kernel_ms"] for s in stats)
     kern_n = sum(s["timed_launches"] for s in stats)
-    achieved = total / (kern_ms / 1e3) / 1e9 / N if kern_ms > 0 else None    # per GPU
+    # per GPU: all GPUs' useful bytes over the sum of their gather-kernel durations
+    achieved = total / (kern_ms / 1e3) / 1e9 if kern_ms > 0 else None
     launches = sum(s["kernel_launches"] for s in stats)
     shared = any(s.get("share_gathers") for s in stats)
     plan_label = table.plan + ("+share" if shared else "")
@@ -1020,7 +1043,7 @@ def run_box(args, spec, dist=None):
     e2e = None
     if not args.no_e2e:
         start = threading.Barrier(N)
-        er = run_threads(N, lambda g: (torch.cuda.set_device(g), workers[g].e2e(start))[1])
+        er = run_threads(N, lambda g: (torch.cuda.set_device(dev_of(g)), workers[g].e2e(start))[1])
         eb = sum(r["bytes"] for r in er)
         e2e = {"value": round(eb / max(r["e_sec"] for r in er) / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": int(sum(r["h2d"] for r in er) / args.steps),
@@ -1035,7 +1058,7 @@ def run_box(args, spec, dist=None):
     # NCCL all-reduce smoke (N > 1, untimed, off the gather path; SURVEY §2.3 ii): one
     # single-process multi-GPU all-reduce over NVLink/NVSwitch
     ar = None
-    if N > 1 and not args.no_allreduce_smoke:
+    if N > 1 and not args.no_allreduce_smoke and not args.oversubscribe:
         import torch.cuda.nccl as nccl
         bufs = []
         for g in range(N):
@@ -1075,7 +1098,9 @@ def run_box(args, spec, dist=None):
         "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (self-identifying fp32-row table, GraphSAGE-shaped index lists)",
         "config": cfg,
-        "harness": "threads: one process drives all GPUs (one host thread each) over one table",
+        "harness": "threads: one process drives all GPUs (one host thread each) over one table"
+                   + (f" (--oversubscribe: {N} workers on {ndev} device(s), a harness test, not "
+                      f"a scaling measurement)" if args.oversubscribe and ndev < N else ""),
         "step_ms": step_stats(all_ms),
         "per_gpu_gbs": [round(x, 3) for x in per_gpu],
         "transferred_gbs_sector_floor": round(value * sect_ratio, 3) if sect_ratio else None,
@@ -1409,6 +1434,9 @@ def main(argv=None):
                          "procs: one process per GPU (torchrun ranks; --coop, --sample gpu)")
     ap.add_argument("--dry-run", action="store_true",
                     help="harness test without a GPU: numpy stand-in for the GPU arm")
+    ap.add_argument("--oversubscribe", action="store_true",
+                    help="harness test: GPU worker g runs on device g %% device_count (N workers "
+                         "on fewer GPUs); no all-reduce smoke")
     ap.add_argument("--seed", type=int, default=2101)
     ap.add_argument("--plan", default="", help="comma list passed to ut_set_plan (A/B runs)")
     ap.add_argument("--max-lists", type=int, default=64, help="distinct minibatches per rank")
@@ -1448,7 +1476,7 @@ def main(argv=None):
         raise SystemExit("--warmup must be >= 3")
     if args.gpus < 1:
         raise SystemExit("--gpus must be >= 1")
-    if args.coop != "off" or args.sample != "cpu" or args.presort:
+    if args.coop != "off" or args.sample != "cpu":
         args.harness = "procs"
     spec = workload_spec(args.config)
     if args.reverse_fanouts and spec["kind"] == "graphsage":

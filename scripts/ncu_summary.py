@@ -64,7 +64,8 @@ def traffic(csv_path, bench_path, out_path):
     line = json.loads([x for x in open(bench_path).read().splitlines() if x.startswith("{")][-1])
     cfg = line["config"]
     rec = {
-        "plan": line["plan"], "table_memory": line.get("table_memory"), "launches": n,
+        "plan": line["plan"], "table_memory": (line.get("table_memory") or "").split(" ")[0] or None,
+        "launches": n,
         "kernel": launches[0]["kernel"] if n else None,
         "hbm_bytes_per_launch": round(avg("dram__bytes_read.sum") + avg("dram__bytes_write.sum")),
         "hbm_read_bytes_per_launch": round(avg("dram__bytes_read.sum")),
@@ -72,6 +73,7 @@ def traffic(csv_path, bench_path, out_path):
         "sysmem_bytes_per_launch": round(32 * avg("syslts__t_sectors_aperture_sysmem_op_read.sum")),
         "sysmem_requests_per_launch": round(avg("syslts__t_requests_aperture_sysmem_op_read.sum")),
         "pcie_read_bytes_per_launch": round(avg("pcie__read_bytes.sum")),
+        "pcie_write_bytes_per_launch": round(avg("pcie__write_bytes.sum")),
         "ncu_ns_per_launch": round(avg("gpu__time_duration.sum")),
         "algorithmic_bytes_per_launch": round(cfg["rows_per_step_per_gpu"] * cfg["row_bytes"]),
         "source": f"ncu per-launch metrics of the gather kernels in bench.py's NVTX 'timed' range "

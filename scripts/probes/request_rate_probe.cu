@@ -174,7 +174,38 @@ int main(int argc, char** argv) {
         run(P, PLAIN, blocks, U);
   // 3) a 256-B pair of lines: plain loads, L2::256B promotion, bulk prefetch to L2 first
   for (int mode : {PAIR, PROMOTE256, PREFETCH256}) run(256, mode, sms * 8, 4);
-  // 4) calibration kernels (ncu reads pcie__read_bytes / pcie__write_bytes of these)
+  // 4) locality: the same random single-line requests confined to a window of the table, and
+  //    the full-table list sorted by address (what a reorder stage would give)
+  auto label = [&](const char* what) {
+    printf("{\"probe\": \"locality\", \"case\": \"%s\"}\n", what);
+  };
+  for (uint64_t win : {1ull << 24, 1ull << 26, 1ull << 28, 1ull << 30, 1ull << 32}) {
+    if (win > bytes) break;
+    std::vector<uint64_t> w(n);
+    for (uint64_t i = 0; i < n; ++i) w[i] = lines[i] % (win / 128);
+    CK(cudaMemcpy(dl, w.data(), n * 8, cudaMemcpyHostToDevice));
+    char buf[64];
+    snprintf(buf, sizeof buf, "window_%llu_MiB", (unsigned long long)(win >> 20));
+    label(buf);
+    run(128, PLAIN, sms * 8, 4);
+    run(64, PLAIN, sms * 8, 4);
+  }
+  {
+    std::vector<uint64_t> srt = lines;
+    std::sort(srt.begin(), srt.end());
+    CK(cudaMemcpy(dl, srt.data(), n * 8, cudaMemcpyHostToDevice));
+    label("sorted_full_table");
+    run(128, PLAIN, sms * 8, 4);
+    run(64, PLAIN, sms * 8, 4);
+    // sorted, but a request every 4th line only (sparser than 1 line per 4 KiB page)
+    for (uint64_t i = 0; i < n; ++i) srt[i] = (i * 37) % nlines;
+    std::sort(srt.begin(), srt.end());
+    CK(cudaMemcpy(dl, srt.data(), n * 8, cudaMemcpyHostToDevice));
+    label("strided_37_lines_sorted");
+    run(128, PLAIN, sms * 8, 4);
+    CK(cudaMemcpy(dl, lines.data(), n * 8, cudaMemcpyHostToDevice));
+  }
+  // 5) calibration kernels (ncu reads pcie__read_bytes / pcie__write_bytes of these)
   const uint64_t cal = 256ull << 20;
   uint8_t* hw;
   CK(cudaHostAlloc(&hw, cal, cudaHostAllocMapped));

@@ -171,3 +171,19 @@ def test_bench_box_harness_tiny():
     assert line["table_memory"].startswith("managed")
     assert line["gpu_launches"] >= 3 and line["value"] > 0
     assert line["step_ms"]["n"] == 3
+
+
+@pytest.mark.timeout(600)
+def test_bench_box_harness_two_workers_one_gpu():
+    """The N > 1 path of the box harness (two GPU worker threads, one table, per-worker parity,
+    sum/max reductions) on this one-GPU pool: --oversubscribe maps both workers to device 0."""
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--oversubscribe", "--config", "products", "--steps", "3", "--warmup", "3",
+                        "--no-cpu", "--no-e2e", "--max-lists", "6"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = json.loads([l for l in p.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["parity_checked"] is True
+    assert line["parity_lists_checked"] >= 4 and len(line["per_gpu_gbs"]) == 2
+    assert "oversubscribe" in line["harness"]
+    assert line["step_ms"]["n"] == 6 and line["roofline"]["frac"] > 0
