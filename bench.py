@@ -810,10 +810,19 @@ class BoxWorker:
             self.flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
         self.stream.synchronize()
 
+    coop = None      # --coop device: this GPU's rank of the in-process cooperative gather
+
     def gather(self, k: int) -> int:
         l = self.idx[k % len(self.idx)]
-        self.table.gather(l, out=self.out[: l.numel() * self.rb], stream=self.stream)
+        if self.coop is not None:
+            self.coop.gather(l, out=self.out[: l.numel() * self.rb], stream=self.stream)
+        else:
+            self.table.gather(l, out=self.out[: l.numel() * self.rb], stream=self.stream)
         return l.numel() * self.rb
+
+    def error_pos(self) -> int:
+        return (self.coop.error_pos(self.stream) if self.coop is not None
+                else self.table.error_pos(self.stream))
 
     def parity(self, host_addr: int, budget_bytes: int) -> int:
         """Byte-exact check of this GPU's lists against the oracle, outside timing (SURVEY §4
@@ -829,8 +838,7 @@ class BoxWorker:
             self.gather(k)
             self.stream.synchronize()
             got = self.out[: l.size * rb].cpu().numpy()
-            if got.tobytes() != want[: l.size * rb].tobytes() or \
-                    self.table.error_pos(self.stream) != bad:
+            if got.tobytes() != want[: l.size * rb].tobytes() or self.error_pos() != bad:
                 raise SystemExit(f"GPU {self.g}: parity failure on minibatch {k}")
             checked += 1
             total += l.size * rb
@@ -988,6 +996,20 @@ def run_box(args, spec, dist=None):
             table.set_plan(p)
     rb = spec["row_bytes"]
     workers = run_threads(N, lambda g: BoxWorker(dev_of(g), torch, table, spec, lists[g], args))
+    coops = None
+    if args.coop == "device":
+        # the cooperative gather among this process's GPUs (ut_coop_open_local):
+        # each row requested by several GPUs in a step is fetched from the host table once, by
+        # its owner, and exchanged over NVLink peer memory
+        max_n = max(l.size for ls in lists for l in ls)
+
+        def mk(g):
+            torch.cuda.set_device(dev_of(g))
+            return ut.Coop(table, max_n, rank=g, world=N, sync="device", local=True)
+        coops = run_threads(N, mk)
+        run_threads(N, lambda g: (torch.cuda.set_device(dev_of(g)), coops[g].open_local(coops)))
+        for g in range(N):
+            workers[g].coop = coops[g]
 
     # roofline denominators, measured now: each GPU's link alone, then all at once
     ndevs = len({dev_of(g) for g in range(N)})
@@ -1003,6 +1025,8 @@ def run_box(args, spec, dist=None):
     parity_lists = 0
     if args.check:
         budget = (16 << 30) // N
+        if coops is not None:     # every rank takes part in every cooperative step
+            budget = 0            # -> exactly two lists on every GPU
         parity_lists = sum(run_threads(N, lambda g: (torch.cuda.set_device(dev_of(g)),
                                                       workers[g].parity(hb.addr, budget))[1]))
 
@@ -1019,6 +1043,7 @@ def run_box(args, spec, dist=None):
             out.append(table.stats(reset=True))
         return out
     dev_stats()
+    coop0 = [c.stats() for c in coops] if coops is not None else None
     start = threading.Barrier(N)
     res = run_threads(N, lambda g: (torch.cuda.set_device(dev_of(g)), workers[g].timed(start))[1])
     clk = clocks.stop()
@@ -1034,14 +1059,30 @@ def run_box(args, spec, dist=None):
     kern_ms = sum(s["gather_kernel_ms"] for s in stats)
     kern_n = sum(s["timed_launches"] for s in stats)
     # per GPU: all GPUs' useful bytes over the sum of their gather-kernel durations
-    achieved = total / (kern_ms / 1e3) / 1e9 if kern_ms > 0 else None
+    kern_bytes = total
     launches = sum(s["kernel_launches"] for s in stats)
+    if coops is not None:   # the gather kernels fetch the owners' unique rows only
+        coop1 = [c.stats() for c in coops]
+        kern_bytes = sum(b["unique_rows_fetched"] - a["unique_rows_fetched"]
+                         for a, b in zip(coop0, coop1)) * rb
+        launches += sum(b["kernel_launches"] - a["kernel_launches"] for a, b in zip(coop0, coop1))
+    achieved = kern_bytes / (kern_ms / 1e3) / 1e9 if kern_ms > 0 else None
     shared = any(s.get("share_gathers") for s in stats)
     plan_label = table.plan + ("+share" if shared else "")
     all_ms = [m for r in res for m in r["ms"]]
 
+    coop_block = None
+    if coops is not None:
+        cs = [c.stats() for c in coops]
+        req = sum(c["requested_rows"] for c in cs)
+        uniq = sum(c["unique_rows_fetched"] for c in cs)
+        coop_block = {"sync": "device (in-process ranks, ut_coop_open_local)", "ranks": N,
+                      "requested_rows_all_steps": req, "host_rows_all_steps": uniq,
+                      "host_bytes_fraction": round(uniq / max(1, req), 4),
+                      "note": "counters cover parity, warm-up and timed steps; value counts useful "
+                              "rows (n*rb per GPU), the host link moved host_bytes_fraction of them"}
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and coops is None:
         start = threading.Barrier(N)
         er = run_threads(N, lambda g: (torch.cuda.set_device(dev_of(g)), workers[g].e2e(start))[1])
         eb = sum(r["bytes"] for r in er)
@@ -1133,10 +1174,18 @@ def run_box(args, spec, dist=None):
         "cpu_baseline": cpu_base, "py_baseline": py_base, "e2e": e2e,
         "gpu_launches": int(launches), "clocks": clk,
         "parity_checked": bool(args.check), "parity_lists_checked": parity_lists,
-        "register_s": round(reg_s, 3), "allreduce_smoke": ar,
+        "register_s": round(reg_s, 3), "allreduce_smoke": ar, "coop": coop_block,
         "wall_ms_per_step": round(max(r["wall_s"] for r in res) / args.steps * 1e3, 3),
     }
     print(json.dumps(line), flush=True)
+    if coops is not None:
+        for g in range(N):
+            torch.cuda.set_device(dev_of(g))
+            torch.cuda.synchronize()
+        for g in range(N):
+            torch.cuda.set_device(dev_of(g))
+            coops[g].close()
+            workers[g].coop = None
     del workers
     table.close()
     hb.close()
@@ -1476,7 +1525,7 @@ def main(argv=None):
         raise SystemExit("--warmup must be >= 3")
     if args.gpus < 1:
         raise SystemExit("--gpus must be >= 1")
-    if args.coop != "off" or args.sample != "cpu":
+    if args.coop == "host" or args.sample != "cpu":
         args.harness = "procs"
     spec = workload_spec(args.config)
     if args.reverse_fanouts and spec["kind"] == "graphsage":

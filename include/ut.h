@@ -394,6 +394,16 @@ UT_API int ut_coop_export(const ut_coop* c, void* handle_out, uint64_t* region_b
  * (this rank's entry is ignored). Returns UT_OK, UT_EINVAL or UT_ECUDA. */
 UT_API int ut_coop_open(ut_coop* c, const void* handles);
 
+/* In-process form of ut_coop_open, for one process driving several GPUs with one host thread
+ * each (bench.py's box harness over ONE shared table): peers[q] is rank q's handle
+ * (peers[rank] == c), every one created in this process with the same world, max_n, table shape
+ * and form. Peer regions are addressed directly through unified addressing; peer access is
+ * enabled from c's device to each other rank's device (NVLink / NVSwitch P2P; ranks on the same
+ * device share its memory). Call on every rank, with c's device current, before the first step.
+ * Returns UT_OK, UT_EINVAL (NULL handle, ranks or layouts disagree) or UT_ENOTSUP (two devices
+ * without peer access). */
+UT_API int ut_coop_open_local(ut_coop* c, ut_coop* const* peers, int world);
+
 /* Phase 1: send idx_dev[0..n) (device memory, int64, caller-owned, n <= max_n) to the owners.
  * Starts a new step. Asynchronous on `stream`. Returns UT_OK, UT_EINVAL or UT_ECUDA. */
 UT_API int ut_coop_dispatch(ut_coop* c, const int64_t* idx_dev, uint64_t n, ut_stream_t stream);

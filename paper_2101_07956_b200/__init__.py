@@ -36,7 +36,7 @@ ABI = ("ut_register", "ut_gather", "ut_gather_host", "ut_release", "ut_error_pos
        "ut_sample_capacity", "ut_graph_launches", "ut_coop_create", "ut_coop_export",
        "ut_coop_open", "ut_coop_dispatch", "ut_coop_fetch", "ut_coop_combine", "ut_coop_gather",
        "ut_coop_get_stats", "ut_coop_error_pos", "ut_coop_owner", "ut_coop_release",
-       "ut_coop_create_partitioned", "ut_coop_partition_ids")
+       "ut_coop_create_partitioned", "ut_coop_partition_ids", "ut_coop_open_local")
 
 UT_COOP_HANDLE_BYTES = 64
 
@@ -129,6 +129,8 @@ def _load():
     L.ut_coop_export.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint64)]
     L.ut_coop_open.restype = ctypes.c_int
     L.ut_coop_open.argtypes = [vp, vp]
+    L.ut_coop_open_local.restype = ctypes.c_int
+    L.ut_coop_open_local.argtypes = [vp, ctypes.POINTER(vp), ctypes.c_int]
     L.ut_coop_dispatch.restype = ctypes.c_int
     L.ut_coop_dispatch.argtypes = [vp, vp, u64, vp]
     L.ut_coop_fetch.restype = ctypes.c_int
@@ -316,6 +318,11 @@ def ut_coop_open(c: int, handles: bytes) -> None:
     _check(_lib.ut_coop_open(c, handles))
 
 
+def ut_coop_open_local(c: int, peers: list[int]) -> None:
+    arr = (ctypes.c_void_p * len(peers))(*peers)
+    _check(_lib.ut_coop_open_local(c, arr, len(peers)))
+
+
 def ut_coop_dispatch(c: int, idx_dev: int, n: int, stream: int = 0) -> None:
     _check(_lib.ut_coop_dispatch(c, idx_dev, n, stream))
 
@@ -493,9 +500,13 @@ class Coop:
     sync="host": dispatch / fetch / combine with a stream sync and a group barrier between."""
 
     def __init__(self, table: Table, max_n: int, group=None, rank: int | None = None,
-                 world: int | None = None, sync: str = "device", rows: int | None = None):
+                 world: int | None = None, sync: str = "device", rows: int | None = None,
+                 local: bool = False):
         """rows: None — `table` is the whole shared table; else the whole table's row count and
-        `table` is this rank's partition (rows ut.Coop.partition_ids(rows, rb, world, rank))."""
+        `table` is this rank's partition (rows ut.Coop.partition_ids(rows, rb, world, rank)).
+        local: every rank lives in THIS process (one host thread per GPU, each creating its rank
+        with its device current); no process group is used — call `open_local` on every rank
+        with all ranks' Coop objects before the first step (sync="device" only)."""
         import torch.distributed as dist
         if world is None:
             world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -509,7 +520,9 @@ class Coop:
             self.handle = ut_coop_create(table.handle, world, rank, self.max_n)
         else:
             self.handle = ut_coop_create_partitioned(table.handle, self.rows, world, rank, self.max_n)
-        if world > 1:
+        if local:
+            assert sync == "device", "in-process ranks synchronise on the device"
+        elif world > 1:
             # every rank must agree on the layout of the symmetric regions it is about to map
             mine = (ut_coop_export(self.handle),
                     (world, self.max_n, self.rows, table.row_bytes, rows is not None))
@@ -522,6 +535,11 @@ class Coop:
                                          f"{sorted(shapes)}")
             ut_coop_open(self.handle, b"".join(h[0] for h in allh))
             dist.barrier(group=group)
+
+    def open_local(self, ranks: list["Coop"]) -> None:
+        """Map the other in-process ranks' regions (ut_coop_open_local); this rank's device must
+        be current."""
+        ut_coop_open_local(self.handle, [r.handle for r in ranks])
 
     @staticmethod
     def partition_ids(rows: int, row_bytes: int, world: int, rank: int):

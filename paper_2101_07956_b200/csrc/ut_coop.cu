@@ -458,6 +458,39 @@ int ut_coop_open(ut_coop* c, const void* handles) {
   return UT_OK;
 }
 
+int ut_coop_open_local(ut_coop* c, ut_coop* const* peers, int world) {
+  if (!c || !peers) return set_err(UT_EINVAL, "coop or peers is NULL");
+  if (world != c->world) return set_err(UT_EINVAL, "world %d != the coop's %d", world, c->world);
+  if (peers[c->rank] != c) return set_err(UT_EINVAL, "peers[%d] is not this rank's handle", c->rank);
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != c->dev) return set_err(UT_EINVAL, "current device %d is not the coop's device %d", cur, c->dev);
+  for (int q = 0; q < world; ++q) {
+    const ut_coop* p = peers[q];
+    if (!p) return set_err(UT_EINVAL, "peers[%d] is NULL", q);
+    if (p->world != world || p->rank != q || p->cap != c->cap || p->rows != c->rows ||
+        p->rb != c->rb || p->partitioned != c->partitioned || p->L.total != c->L.total)
+      return set_err(UT_EINVAL, "rank %d disagrees on (world, rank, max_n, rows, row_bytes, form)", q);
+  }
+  for (int q = 0; q < world; ++q) {
+    if (q == c->rank) continue;
+    const ut_coop* p = peers[q];
+    if (p->dev != c->dev) {
+      int ok = 0;
+      cudaDeviceCanAccessPeer(&ok, c->dev, p->dev);
+      if (!ok) return set_err(UT_ENOTSUP, "device %d cannot access device %d (no P2P)", c->dev, p->dev);
+      cudaError_t e = cudaDeviceEnablePeerAccess(p->dev, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (e != cudaSuccess) return cuda_err(e, "cudaDeviceEnablePeerAccess");
+    }
+    c->peer_host[q] = p->region;    // not IPC-opened: ut_coop_release leaves it to its owner
+    c->opened[q] = false;
+  }
+  cudaError_t e = cudaMemcpy(c->peers_dev, c->peer_host, sizeof(uint8_t*) * c->world, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_err(e, "cudaMemcpy(peer table)");
+  return UT_OK;
+}
+
 int ut_coop_dispatch(ut_coop* c, const int64_t* idx_dev, uint64_t n, ut_stream_t stream) {
   if (!c) return set_err(UT_EINVAL, "coop is NULL");
   if (n > c->cap) return set_err(UT_EINVAL, "n = %llu exceeds max_n = %llu", (unsigned long long)n,

@@ -187,3 +187,70 @@ def test_bench_box_harness_two_workers_one_gpu():
     assert line["parity_lists_checked"] >= 4 and len(line["per_gpu_gbs"]) == 2
     assert "oversubscribe" in line["harness"]
     assert line["step_ms"]["n"] == 6 and line["roofline"]["frac"] > 0
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world", [2, 3])
+def test_coop_in_process_ranks(world):
+    """ut_coop_open_local: `world` ranks of the cooperative gather in ONE process (a host thread
+    each, here all on device 0) over one managed table; every rank's rows equal the oracle's and
+    the owners fetch each requested row from host memory once per step."""
+    rows, rb = 60_000, 400
+    with ut.Table.create(rows, rb, "managed") as t:
+        workloads.fill_table(t.host_addr, rows, rb, 701)
+        lists = [workloads.uniform_idx(20_000 + 13 * r, rows // 4, 710 + r) for r in range(world)]
+        lists[0][5] = rows + 2                       # one out-of-range id on rank 0
+        wants = [oracle.gather(t.host_addr, rows, rb, l) for l in lists]
+        max_n = max(l.size for l in lists)
+        coops = [None] * world
+
+        def mk(r):
+            torch.cuda.set_device(0)
+            coops[r] = ut.Coop(t, max_n, rank=r, world=world, sync="device", local=True)
+
+        th = [threading.Thread(target=mk, args=(r,)) for r in range(world)]
+        [x.start() for x in th]
+        [x.join() for x in th]
+        for c in coops:
+            c.open_local(coops)
+        outs, errs = [None] * world, []
+
+        def step(r):
+            try:
+                torch.cuda.set_device(0)
+                s = torch.cuda.Stream()
+                idx = torch.from_numpy(lists[r]).cuda()
+                for _ in range(3):                      # several steps: parity double-buffering
+                    o = coops[r].gather(idx, stream=s)
+                s.synchronize()
+                outs[r] = (o.cpu().numpy(), coops[r].error_pos(s))
+            except Exception as e:   # pragma: no cover
+                errs.append(repr(e))
+
+        th = [threading.Thread(target=step, args=(r,)) for r in range(world)]
+        [x.start() for x in th]
+        [x.join() for x in th]
+        assert not errs, errs
+        for r in range(world):
+            got, bad = outs[r]
+            assert got.tobytes() == wants[r][0].tobytes(), r
+            assert bad == wants[r][1]
+        valid = np.concatenate([l[(l >= 0) & (l < rows)] for l in lists])
+        fetched = sum(c.stats()["last_unique_rows"] for c in coops)
+        assert fetched == np.unique(valid).size          # each requested row crossed the link once
+        for c in coops:
+            c.close()
+
+
+@pytest.mark.timeout(600)
+def test_bench_box_harness_coop_two_workers():
+    """bench.py --coop device in the box harness (two in-process ranks on this one GPU)."""
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--oversubscribe", "--coop", "device", "--config", "products", "--steps", "3",
+                        "--warmup", "3", "--no-cpu", "--max-lists", "6"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = json.loads([l for l in p.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["parity_checked"] is True
+    assert line["parity_lists_checked"] == 4
+    assert 0.5 < line["coop"]["host_bytes_fraction"] < 1.0
