@@ -157,7 +157,11 @@ def box_throughput(dist, nbytes: int, dev_ms: float, wall_s: float, launches: in
 
 # ---- measurement helpers -----------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 100 ms from warm-up to the end of timing."""
+    """nvidia-smi clocks / throttle reasons, sampled every 50 ms. start() returns only once the
+    first sample has arrived, so nvidia-smi's own start-up (driver queries, ~1 s) is over before
+    anything is timed; mark() brackets the timed region, and the line reports the samples inside
+    it (`samples_timed`) next to all samples from the start of warm-up (`samples`). The median
+    and the reasons cover warm-up + timing (the timed region alone is ~0.1 s on the default)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -165,29 +169,38 @@ class ClockSampler:
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index if isinstance(gpu_index, int) else ",".join(str(g) for g in gpu_index)
-        self.lines: list[str] = []
+        self.lines: list[tuple[float, str]] = []
         self.proc = None
         self.thread = None
+        self.window = [None, None]
+        self.first = threading.Event()
 
-    def start(self):
+    def start(self, wait_s: float = 10.0):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except (OSError, FileNotFoundError):
             self.proc = None
             return
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
+        self.first.wait(wait_s)
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+            self.first.set()
+
+    def mark(self, which: int) -> None:
+        """0: timed region starts, 1: it ends."""
+        self.window[which] = time.perf_counter()
 
     def stop(self) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.06)          # one more sample after the timed region
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -195,9 +208,10 @@ class ClockSampler:
             self.proc.kill()
         if self.thread:
             self.thread.join(timeout=2)
-        sm, mx, reasons = [], [], set()
+        sm, mx, reasons, timed = [], [], set(), 0
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in self.lines:
+        t0, t1 = self.window
+        for ts, l in self.lines:
             f = [x.strip() for x in l.split(",")]
             if len(f) < 9:
                 continue
@@ -206,12 +220,15 @@ class ClockSampler:
                 mx.append(float(f[2]))
             except ValueError:
                 continue
+            if t0 is not None and t1 is not None and t0 <= ts <= t1 + 0.06:
+                timed += 1
             for k, v in zip(names, f[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(k)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "samples_timed": timed,
+                "window": "warm-up start to timing end, 50-ms nvidia-smi samples"}
 
 
 def h2d_ceiling(torch, nbytes: int = 1 << 30, reps: int = 10, stream=None, host=None) -> float:
@@ -551,6 +568,7 @@ def run_procs(args, spec, dist):
     torch.cuda.synchronize()
     # NVTX range "timed": ncu's --nvtx --nvtx-include "timed/" profiles exactly these launches
     torch.cuda.nvtx.range_push("timed")
+    clocks.mark(0)
     t0 = time.perf_counter()
     if sampler is not None and args.pipeline:
         # sample minibatch k+1 (its own stream) while minibatch k is gathered: the whole loop is
@@ -577,6 +595,7 @@ def run_procs(args, spec, dist):
         nbytes += sampler.device_rows() * rb
     dist.barrier()
     wall = time.perf_counter() - t0
+    clocks.mark(1)
     clk = clocks.stop()
     st = table.stats(reset=True)
     table.set_plan("timing=off")
@@ -1045,7 +1064,9 @@ def run_box(args, spec, dist=None):
     dev_stats()
     coop0 = [c.stats() for c in coops] if coops is not None else None
     start = threading.Barrier(N)
+    clocks.mark(0)
     res = run_threads(N, lambda g: (torch.cuda.set_device(dev_of(g)), workers[g].timed(start))[1])
+    clocks.mark(1)
     clk = clocks.stop()
     stats = dev_stats()
     table.set_plan("timing=off")
