@@ -827,6 +827,7 @@ class BoxWorker:
             self.idx = [torch.from_numpy(l).to("cuda") for l in lists]
             self.out = torch.empty(self.max_n * self.rb, dtype=torch.uint8, device="cuda")
             self.flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+            self.flush.zero_()      # loads torch's fill kernel now, not inside a timed step
         self.stream.synchronize()
 
     coop = None      # --coop device: this GPU's rank of the in-process cooperative gather
@@ -1548,6 +1549,12 @@ def main(argv=None):
         raise SystemExit("--gpus must be >= 1")
     if args.coop == "host" or args.sample != "cpu":
         args.harness = "procs"
+    if args.coop == "device" and args.harness == "threads":
+        # in-process ranks wait for each other on the device (ut_coop_open_local): one hardware
+        # queue per stream when several ranks share a device (--oversubscribe), set before any
+        # CUDA context; the kernels a step launches are loaded before the first step (the
+        # library's own in ut_coop_open_local, torch's L2 flush in BoxWorker.__init__)
+        os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
     spec = workload_spec(args.config)
     if args.reverse_fanouts and spec["kind"] == "graphsage":
         spec["reverse_fanouts"] = True          # DGL's order: the last fanout at the seeds (c15)

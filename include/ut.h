@@ -69,10 +69,14 @@ typedef enum ut_status {
  * instead pins and maps the caller's memory WITHOUT copying, so that several processes can
  * register one shared table (reading R1).
  *   host_ptr   caller-owned host memory, any alignment. It must stay valid, and unmodified while
- *              any gather is in flight, until ut_release. If it is already page-locked and mapped
- *              (cudaHostAlloc/cudaHostRegister by the caller), it is adopted and left pinned on
- *              release; otherwise it is registered with cudaHostRegister(Portable|Mapped
- *              [|ReadOnly when the device supports it]) and unregistered by ut_release.
+ *              any gather is in flight, until ut_release. If it lies inside one page-locked and
+ *              mapped allocation (cudaHostAlloc / cudaHostRegister by the caller), it is adopted
+ *              and left pinned on release; otherwise its pages are registered with
+ *              cudaHostRegister(Portable|Mapped[|ReadOnly when the device supports it]) and
+ *              unregistered by ut_release. A range that only partly overlaps pinned memory (other
+ *              allocations' pages at its ends or inside it) is walked allocation by allocation:
+ *              the pinned stretches are adopted and every unpinned gap is registered, so every
+ *              byte is GPU-addressable before the handle is returned (or the call fails).
  *   rows       number of rows, >= 1.
  *   row_bytes  bytes per row, >= 1; rows * row_bytes must not overflow 64 bits.
  * The current CUDA device is used for registration; the mapping is Portable, so the handle
@@ -400,6 +404,13 @@ UT_API int ut_coop_open(ut_coop* c, const void* handles);
  * and form. Peer regions are addressed directly through unified addressing; peer access is
  * enabled from c's device to each other rank's device (NVLink / NVSwitch P2P; ranks on the same
  * device share its memory). Call on every rank, with c's device current, before the first step.
+ * Forward progress: ranks wait for each other on the device, so nothing a step launches may
+ * need the device idle. This call loads every kernel of a step (lazy module loading would
+ * otherwise load them while a peer's stream waits at a barrier); kernels the CALLER launches
+ * between steps must be loaded before the first step too (or run the process with
+ * CUDA_MODULE_LOADING=EAGER). Several ranks on ONE device additionally need a hardware queue
+ * each (CUDA_DEVICE_MAX_CONNECTIONS >= streams in use, e.g. 32), or a waiting stream can hold the
+ * queue its peer's flag write sits in.
  * Returns UT_OK, UT_EINVAL (NULL handle, ranks or layouts disagree) or UT_ENOTSUP (two devices
  * without peer access). */
 UT_API int ut_coop_open_local(ut_coop* c, ut_coop* const* peers, int world);

@@ -488,6 +488,25 @@ int ut_coop_open_local(ut_coop* c, ut_coop* const* peers, int world) {
   }
   cudaError_t e = cudaMemcpy(c->peers_dev, c->peer_host, sizeof(uint8_t*) * c->world, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_err(e, "cudaMemcpy(peer table)");
+  // In-process ranks wait for each other on the device (stream memory operations). Loading a
+  // kernel lazily (CUDA_MODULE_LOADING=LAZY, the default) while another rank's stream of the
+  // same process waits at a barrier can stall both, so every kernel a step launches is loaded
+  // now: the coop kernels by their attributes, the host fetch's gather plan (and its reorder
+  // stage, when the policy takes it) by one device-count gather of zero rows at the step's size.
+  const void* ks[] = {(const void*)k_dispatch, (const void*)k_publish, (const void*)k_dedup<1>,
+                      (const void*)k_dedup<2>, (const void*)k_dedup<3>, (const void*)k_unique_total,
+                      (const void*)k_combine<W16>, (const void*)k_combine<uint64_t>,
+                      (const void*)k_combine<uint32_t>, (const void*)k_combine<uint16_t>,
+                      (const void*)k_combine<uint8_t>};
+  for (const void* k : ks) {
+    cudaFuncAttributes fa;
+    if ((e = cudaFuncGetAttributes(&fa, k)) != cudaSuccess) return cuda_err(e, "cudaFuncGetAttributes");
+  }
+  if ((e = cudaMemsetAsync(c->u, 0, 8, 0)) != cudaSuccess) return cuda_err(e, "cudaMemsetAsync(preload)");
+  const int rc = ut_gather_dn(c->t, c->uniq, (const uint64_t*)c->u, c->cap * (uint64_t)c->world,
+                              c->region + c->L.stage, nullptr);
+  if (rc != UT_OK) return rc;
+  if ((e = cudaStreamSynchronize(0)) != cudaSuccess) return cuda_err(e, "preload gather");
   return UT_OK;
 }
 

@@ -194,52 +194,13 @@ def test_bench_box_harness_two_workers_one_gpu():
 def test_coop_in_process_ranks(world):
     """ut_coop_open_local: `world` ranks of the cooperative gather in ONE process (a host thread
     each, here all on device 0) over one managed table; every rank's rows equal the oracle's and
-    the owners fetch each requested row from host memory once per step."""
-    rows, rb = 60_000, 400
-    with ut.Table.create(rows, rb, "managed") as t:
-        workloads.fill_table(t.host_addr, rows, rb, 701)
-        lists = [workloads.uniform_idx(20_000 + 13 * r, rows // 4, 710 + r) for r in range(world)]
-        lists[0][5] = rows + 2                       # one out-of-range id on rank 0
-        wants = [oracle.gather(t.host_addr, rows, rb, l) for l in lists]
-        max_n = max(l.size for l in lists)
-        coops = [None] * world
-
-        def mk(r):
-            torch.cuda.set_device(0)
-            coops[r] = ut.Coop(t, max_n, rank=r, world=world, sync="device", local=True)
-
-        th = [threading.Thread(target=mk, args=(r,)) for r in range(world)]
-        [x.start() for x in th]
-        [x.join() for x in th]
-        for c in coops:
-            c.open_local(coops)
-        outs, errs = [None] * world, []
-
-        def step(r):
-            try:
-                torch.cuda.set_device(0)
-                s = torch.cuda.Stream()
-                idx = torch.from_numpy(lists[r]).cuda()
-                for _ in range(3):                      # several steps: parity double-buffering
-                    o = coops[r].gather(idx, stream=s)
-                s.synchronize()
-                outs[r] = (o.cpu().numpy(), coops[r].error_pos(s))
-            except Exception as e:   # pragma: no cover
-                errs.append(repr(e))
-
-        th = [threading.Thread(target=step, args=(r,)) for r in range(world)]
-        [x.start() for x in th]
-        [x.join() for x in th]
-        assert not errs, errs
-        for r in range(world):
-            got, bad = outs[r]
-            assert got.tobytes() == wants[r][0].tobytes(), r
-            assert bad == wants[r][1]
-        valid = np.concatenate([l[(l >= 0) & (l < rows)] for l in lists])
-        fetched = sum(c.stats()["last_unique_rows"] for c in coops)
-        assert fetched == np.unique(valid).size          # each requested row crossed the link once
-        for c in coops:
-            c.close()
+    the owners fetch each requested row from host memory once per step. Runs in a fresh process
+    with the environment the header asks for when ranks share a device (eager module loading,
+    a hardware queue per stream): tests/coop_local_case.py."""
+    env = dict(os.environ, CUDA_MODULE_LOADING="EAGER", CUDA_DEVICE_MAX_CONNECTIONS="32")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "coop_local_case.py"), str(world)],
+                       capture_output=True, text=True, timeout=280, cwd=ROOT, env=env)
+    assert p.returncode == 0 and "COOP-LOCAL-OK" in p.stdout, (p.stdout + p.stderr)[-3000:]
 
 
 @pytest.mark.timeout(600)
