@@ -1122,20 +1122,24 @@ def run_box(args, spec, dist=None):
     # single-process multi-GPU all-reduce over NVLink/NVSwitch
     ar = None
     if N > 1 and not args.no_allreduce_smoke and not args.oversubscribe:
-        import torch.cuda.nccl as nccl
-        bufs = []
-        for g in range(N):
-            with torch.cuda.device(g):
-                bufs.append(torch.full((1 << 20,), float(g + 1), dtype=torch.float32, device="cuda"))
-        t1 = time.perf_counter()
-        nccl.all_reduce(bufs)
-        for g in range(N):
-            torch.cuda.synchronize(g)
-        want = N * (N + 1) / 2
-        ar = {"ok": all(bool((b == want).all().item()) for b in bufs), "bytes": bufs[0].numel() * 4,
-              "ms": round((time.perf_counter() - t1) * 1e3, 3),
-              "backend": "nccl (torch.cuda.nccl, one process, all GPUs)", "gpus": N}
-        del bufs
+        try:        # context, off the measured path: a failure is reported, not fatal
+            import torch.cuda.nccl as nccl
+            bufs = []
+            for g in range(N):
+                with torch.cuda.device(g):
+                    bufs.append(torch.full((1 << 20,), float(g + 1), dtype=torch.float32,
+                                           device="cuda"))
+            t1 = time.perf_counter()
+            nccl.all_reduce(bufs)
+            for g in range(N):
+                torch.cuda.synchronize(g)
+            want = N * (N + 1) / 2
+            ar = {"ok": all(bool((b == want).all().item()) for b in bufs),
+                  "bytes": bufs[0].numel() * 4, "ms": round((time.perf_counter() - t1) * 1e3, 3),
+                  "backend": "nccl (torch.cuda.nccl, one process, all GPUs)", "gpus": N}
+            del bufs
+        except Exception as e:  # noqa: BLE001
+            ar = {"ok": False, "error": f"{type(e).__name__}: {e}"[:300]}
 
     dram = None
     if not args.no_cpu:

@@ -1240,7 +1240,8 @@ int ut_gather_host(const ut_table* ct, const int64_t* idx_host, uint64_t n, void
   cudaGetLastError();
   // (measured: with a managed table the copy-engine pipeline below is faster — papers-shaped
   // 32.6 vs 19.1 GB/s — while for registered / pinned tables direct stores win, 29 vs 20)
-  if (out_mapped && !getenv("UT_HOST_PIPELINE") && t->alloc_kind != UT_ALLOC_MANAGED) {
+  static const bool force_direct = getenv("UT_HOST_DIRECT") != nullptr;   // A/B knob
+  if (out_mapped && !getenv("UT_HOST_PIPELINE") && (t->alloc_kind != UT_ALLOC_MANAGED || force_direct)) {
     if (s->idx_cap < n) {
       if (s->idx_all) cudaFree(s->idx_all);
       s->idx_all = nullptr;
