@@ -902,7 +902,7 @@ class BoxWorker:
         probe = torch.empty(1, dtype=torch.int64, pin_memory=True)
         for s in range(min(2, len(idx_host))):
             self.table.gather_host(idx_host[s], out_host=out_host, stream=self.stream)
-        r = {"e_sec": 0.0, "f_sec": 0.0, "bytes": 0, "h2d": 0, "d2h": 0}
+        r = {"e_sec": 0.0, "f_sec": 0.0, "bytes": 0, "h2d": 0, "d2h": 0, "e_ms": [], "f_ms": []}
         start.wait()
         for s in range(args.steps):
             ih = idx_host[(args.warmup + s) % len(idx_host)]
@@ -911,7 +911,8 @@ class BoxWorker:
             self.stream.synchronize()
             t1 = time.perf_counter()
             self.table.gather_host(ih, out_host=out_host, stream=self.stream)
-            r["e_sec"] += time.perf_counter() - t1
+            r["e_ms"].append((time.perf_counter() - t1) * 1e3)
+            r["e_sec"] += r["e_ms"][-1] / 1e3
             r["bytes"] += ih.numel() * rb
             r["h2d"] += ih.numel() * 8
             r["d2h"] += ih.numel() * rb
@@ -927,7 +928,8 @@ class BoxWorker:
                 res = self.table.gather(idx_d, out=self.out[: ih.numel() * rb], stream=self.stream)
                 probe.copy_(res[:8].view(torch.int64), non_blocking=True)
             self.stream.synchronize()
-            r["f_sec"] += time.perf_counter() - t1
+            r["f_ms"].append((time.perf_counter() - t1) * 1e3)
+            r["f_sec"] += r["f_ms"][-1] / 1e3
         del out_host, idx_host
         return r
 
@@ -1112,9 +1114,11 @@ def run_box(args, spec, dist=None):
                "h2d_bytes_per_step": int(sum(r["h2d"] for r in er) / args.steps),
                "d2h_bytes_per_step": int(sum(r["d2h"] for r in er) / args.steps),
                "path": "ut_gather_host on every GPU at once: pinned host idx in, pinned host rows out",
+               "step_ms": step_stats([m for r in er for m in r["e_ms"]]),
                "to_hbm": {"value": round(eb / max(r["f_sec"] for r in er) / 1e9, 3), "unit": "GB/s",
                           "h2d_bytes_per_step": int(sum(r["h2d"] for r in er) / args.steps),
                           "d2h_bytes_per_step": 8 * N,
+                          "step_ms": step_stats([m for r in er for m in r["f_ms"]]),
                           "path": "Table.gather with a pinned host idx: idx H2D, gather into HBM, "
                                   "8-B read-back of the result (the paper's Listing 2 pipeline)"}}
 

@@ -145,9 +145,9 @@ UT_API int ut_gather_dn(const ut_table* t, const int64_t* idx_dev, const uint64_
  * ut_gather_host — the same gather from and to HOST buffers (the end-to-end form).
  *   idx_host  n int64 row ids in host memory (page-locked for full speed; caller-owned).
  *   out_host  >= n*rb bytes of host memory (caller-owned).
- * If out_host is page-locked and mapped (cudaHostAlloc / cudaHostRegister'ed) and the table is
- * not a managed one, idx is copied to the device and the gather kernel stores the rows straight
- * into out_host over the link (one pass, no HBM round trip). Otherwise rows are gathered in
+ * If out_host is page-locked and mapped (cudaHostAlloc / cudaHostRegister'ed), idx is copied to
+ * the device and the gather kernel stores the rows straight into out_host over the link (one
+ * pass, no HBM round trip). Otherwise rows are gathered in
  * chunks into library-owned device
  * scratch and copied back by the copy engine on a second stream, overlapping the two link
  * directions (UT_HOST_PIPELINE=1 forces this path). Device scratch is owned by the table and

@@ -1238,10 +1238,10 @@ int ut_gather_host(const ut_table* ct, const int64_t* idx_host, uint64_t n, void
       out_mapped = oa.devicePointer;
   }
   cudaGetLastError();
-  // (measured: with a managed table the copy-engine pipeline below is faster — papers-shaped
-  // 32.6 vs 19.1 GB/s — while for registered / pinned tables direct stores win, 29 vs 20)
-  static const bool force_direct = getenv("UT_HOST_DIRECT") != nullptr;   // A/B knob
-  if (out_mapped && !getenv("UT_HOST_PIPELINE") && (t->alloc_kind != UT_ALLOC_MANAGED || force_direct)) {
+  // (measured, round 2, papers-shaped managed table: direct stores 36.7 GB/s host->host vs the
+  // copy-engine pipeline's 32.6 at its best chunk size, 23.8-32.0 over 2-64 MiB chunks,
+  // profiles/r2/r2h/e2e_variants.log; registered tables: direct 29-31 vs 20)
+  if (out_mapped && !getenv("UT_HOST_PIPELINE")) {
     if (s->idx_cap < n) {
       if (s->idx_all) cudaFree(s->idx_all);
       s->idx_all = nullptr;

@@ -215,3 +215,24 @@ def test_bench_box_harness_coop_two_workers():
     assert line["n_gpus"] == 2 and line["parity_checked"] is True
     assert line["parity_lists_checked"] == 4
     assert 0.5 < line["coop"]["host_bytes_fraction"] < 1.0
+
+
+@pytest.mark.parametrize("kind", ["managed", "pinned", "vmm"])
+@pytest.mark.parametrize("rb", [68, 512, 2408])
+def test_gather_host_library_owned_tables(kind, rb):
+    """ut_gather_host's direct path (kernel stores into pinned host output) and its pipeline
+    (pageable output) on every ut_create kind, against the oracle."""
+    rows = 30_000
+    with ut.Table.create(rows, rb, kind) as t:
+        workloads.fill_table(t.host_addr, rows, rb, 800 + rb)
+        idx = workloads.uniform_idx(25_001, rows, 801)
+        idx[11] = -3
+        want, bad = oracle.gather(t.host_addr, rows, rb, idx)
+        idx_h = torch.from_numpy(idx).pin_memory()
+        got = t.gather_host(idx_h)                                 # pinned output: direct
+        assert got.numpy().tobytes() == want.tobytes()
+        assert t.error_pos() == bad == 11
+        out = torch.full((idx.size, rb), 0xAB, dtype=torch.uint8)  # pageable output: pipeline
+        t.gather_host(idx_h, out_host=out)
+        assert out.numpy().tobytes() == want.tobytes()
+        assert t.error_pos() == 11
