@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes
+import gc
 import json
 import multiprocessing as mp
 import os
@@ -900,6 +901,8 @@ class BoxWorker:
         idx_host = [torch.from_numpy(x).pin_memory() for x in self.lists]
         out_host = torch.empty(self.max_n * rb, dtype=torch.uint8, pin_memory=True)
         probe = torch.empty(1, dtype=torch.int64, pin_memory=True)
+        with torch.cuda.stream(self.stream):
+            self.idx_up = torch.empty(self.max_n, dtype=torch.int64, device="cuda")
         for s in range(min(2, len(idx_host))):
             self.table.gather_host(idx_host[s], out_host=out_host, stream=self.stream)
         r = {"e_sec": 0.0, "f_sec": 0.0, "bytes": 0, "h2d": 0, "d2h": 0, "e_ms": [], "f_ms": []}
@@ -924,7 +927,8 @@ class BoxWorker:
             self.stream.synchronize()
             t1 = time.perf_counter()
             with torch.cuda.stream(self.stream):
-                idx_d = ih.to("cuda", non_blocking=True)
+                idx_d = self.idx_up[: ih.numel()]
+                idx_d.copy_(ih, non_blocking=True)
                 res = self.table.gather(idx_d, out=self.out[: ih.numel() * rb], stream=self.stream)
                 probe.copy_(res[:8].view(torch.int64), non_blocking=True)
             self.stream.synchronize()
@@ -1067,9 +1071,12 @@ def run_box(args, spec, dist=None):
     dev_stats()
     coop0 = [c.stats() for c in coops] if coops is not None else None
     start = threading.Barrier(N)
+    gc.collect()
+    gc.disable()          # no collector pauses inside the timed host loops
     clocks.mark(0)
     res = run_threads(N, lambda g: (torch.cuda.set_device(dev_of(g)), workers[g].timed(start))[1])
     clocks.mark(1)
+    gc.enable()
     clk = clocks.stop()
     stats = dev_stats()
     table.set_plan("timing=off")
@@ -1108,7 +1115,14 @@ def run_box(args, spec, dist=None):
     e2e = None
     if not args.no_e2e and coops is None:
         start = threading.Barrier(N)
+        gc.collect()
+        gc.disable()
         er = run_threads(N, lambda g: (torch.cuda.set_device(dev_of(g)), workers[g].e2e(start))[1])
+        gc.enable()
+        if os.environ.get("UT_BENCH_DEBUG"):
+            for g, r in enumerate(er):
+                print(f"e2e gpu{g} host->host ms: {[round(x, 3) for x in r['e_ms']]}", file=sys.stderr)
+                print(f"e2e gpu{g} to_hbm ms: {[round(x, 3) for x in r['f_ms']]}", file=sys.stderr)
         eb = sum(r["bytes"] for r in er)
         e2e = {"value": round(eb / max(r["e_sec"] for r in er) / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": int(sum(r["h2d"] for r in er) / args.steps),
