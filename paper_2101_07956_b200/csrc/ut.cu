@@ -1243,14 +1243,18 @@ int ut_gather_host(const ut_table* ct, const int64_t* idx_host, uint64_t n, void
   // profiles/r2/r2h/e2e_variants.log; registered tables: direct 29-31 vs 20)
   if (out_mapped && !getenv("UT_HOST_PIPELINE")) {
     if (s->idx_cap < n) {
+      // grown geometrically (x1.5, whole MiB): a reallocation synchronises the device, and
+      // minibatch sizes vary by a few percent from step to step
+      const uint64_t want = std::max<uint64_t>(n, s->idx_cap + s->idx_cap / 2);
+      const uint64_t cap = ((want * sizeof(int64_t) + (1u << 20) - 1) >> 20 << 20) / sizeof(int64_t);
       if (s->idx_all) cudaFree(s->idx_all);
       s->idx_all = nullptr;
       s->idx_cap = 0;
-      if (cudaMalloc(&s->idx_all, n * sizeof(int64_t)) != cudaSuccess) {
+      if (cudaMalloc(&s->idx_all, cap * sizeof(int64_t)) != cudaSuccess) {
         cudaGetLastError();
-        return set_err(UT_ENOMEM, "device index scratch of %llu rows", (unsigned long long)n);
+        return set_err(UT_ENOMEM, "device index scratch of %llu rows", (unsigned long long)cap);
       }
-      s->idx_cap = n;
+      s->idx_cap = cap;
     }
     if ((e = cudaMemcpyAsync(s->idx_all, idx_host, n * sizeof(int64_t), cudaMemcpyHostToDevice,
                              st)) != cudaSuccess)
