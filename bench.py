@@ -832,8 +832,12 @@ class BoxWorker:
         self.stream.synchronize()
 
     coop = None      # --coop device: this GPU's rank of the in-process cooperative gather
+    sampler = None   # --sample gpu: this GPU's sampler (GpuSampling, sync mode)
 
     def gather(self, k: int) -> int:
+        if self.sampler is not None:     # sample this step's minibatch on the GPU, then gather
+            with self.torch.cuda.stream(self.stream):
+                return self.sampler.step(k, self.table, self.out) * self.rb
         l = self.idx[k % len(self.idx)]
         if self.coop is not None:
             self.coop.gather(l, out=self.out[: l.numel() * self.rb], stream=self.stream)
@@ -849,6 +853,11 @@ class BoxWorker:
         """Byte-exact check of this GPU's lists against the oracle, outside timing (SURVEY §4
         T2): every list while the rows fit `budget_bytes`, at least two. Returns lists checked."""
         import oracle
+        if self.sampler is not None:     # sampled node list and its rows, both against the oracle
+            with self.torch.cuda.stream(self.stream):
+                if not self.sampler.check(host_addr, self.table, self.out):
+                    raise SystemExit(f"GPU {self.g}: parity failure (GPU sampling + gather)")
+            return 1
         rb = self.rb
         want = np.empty(self.max_n * rb, dtype=np.uint8)
         checked, total = 0, 0
@@ -1023,7 +1032,25 @@ def run_box(args, spec, dist=None):
         for p in args.plan.split(","):
             table.set_plan(p)
     rb = spec["row_bytes"]
+    samplers = None
+    if args.sample == "gpu":
+        # GPU-side neighbour sampling on every GPU from ONE host CSR: each worker
+        # samples its own roots' minibatch, then gathers it (sync mode: one count read per step)
+        assert args.coop == "off", "--sample gpu with --coop: use --harness procs"
+        csr = workloads.CSRGraph(spec["rows"], spec["edges"], seed=seed, threads=0)
+
+        def mk_sampler(g):
+            torch.cuda.set_device(dev_of(g))
+            return GpuSampling(spec, g, N, count, seed, ut, torch, args.graph_indptr, "sync",
+                               csr=csr)
+        samplers = run_threads(N, mk_sampler)
+        lists = run_threads(N, lambda g: (torch.cuda.set_device(dev_of(g)),
+                                          samplers[g].node_lists_for_accounting())[1])
+        timed_lists = [lists[0][(args.warmup + s) % count] for s in range(args.steps)]
     workers = run_threads(N, lambda g: BoxWorker(dev_of(g), torch, table, spec, lists[g], args))
+    if samplers is not None:
+        for g in range(N):
+            workers[g].sampler = samplers[g]
     coops = None
     if args.coop == "device":
         # the cooperative gather among this process's GPUs (ut_coop_open_local):
@@ -1072,6 +1099,9 @@ def run_box(args, spec, dist=None):
         return out
     dev_stats()
     coop0 = [c.stats() for c in coops] if coops is not None else None
+    if samplers is not None:
+        for smp in samplers:
+            smp.mark()
     start = threading.Barrier(N)
     gc.collect()
     gc.disable()          # no collector pauses inside the timed host loops
@@ -1099,6 +1129,8 @@ def run_box(args, spec, dist=None):
         kern_bytes = sum(b["unique_rows_fetched"] - a["unique_rows_fetched"]
                          for a, b in zip(coop0, coop1)) * rb
         launches += sum(b["kernel_launches"] - a["kernel_launches"] for a, b in zip(coop0, coop1))
+    if samplers is not None:
+        launches += sum(smp.timed_launches(args.steps) for smp in samplers)
     achieved = kern_bytes / (kern_ms / 1e3) / 1e9 if kern_ms > 0 else None
     shared = any(s.get("share_gathers") for s in stats)
     plan_label = table.plan + ("+share" if shared else "")
@@ -1115,7 +1147,7 @@ def run_box(args, spec, dist=None):
                       "note": "counters cover parity, warm-up and timed steps; value counts useful "
                               "rows (n*rb per GPU), the host link moved host_bytes_fraction of them"}
     e2e = None
-    if not args.no_e2e and coops is None:
+    if not args.no_e2e and coops is None and samplers is None:
         start = threading.Barrier(N)
         gc.collect()
         gc.disable()
@@ -1221,6 +1253,7 @@ def run_box(args, spec, dist=None):
         "gpu_launches": int(launches), "clocks": clk,
         "parity_checked": bool(args.check), "parity_lists_checked": parity_lists,
         "register_s": round(reg_s, 3), "allreduce_smoke": ar, "coop": coop_block,
+        "sampling": samplers[0].report(args.steps) if samplers is not None else None,
         "wall_ms_per_step": round(max(r["wall_s"] for r in res) / args.steps * 1e3, 3),
     }
     print(json.dumps(line), flush=True)
@@ -1244,10 +1277,13 @@ class GpuSampling:
     N and E (workloads.CSRGraph); each step's 'batch' roots are the rank's slice of a seeded
     permutation."""
 
-    def __init__(self, spec, rank, world, count, seed, ut, torch, indptr="host", mode="sync"):
+    def __init__(self, spec, rank, world, count, seed, ut, torch, indptr="host", mode="sync",
+                 csr=None):
         assert spec["kind"] == "graphsage", "--sample gpu needs a graphsage-shaped config"
         self.torch, self.ut, self.spec = torch, ut, spec
-        self.csr = workloads.CSRGraph(spec["rows"], spec["edges"], seed=seed, threads=0)
+        # csr: one host CSR shared by the box harness's GPU workers (each registers it itself)
+        self.csr = csr if csr is not None else workloads.CSRGraph(spec["rows"], spec["edges"],
+                                                                   seed=seed, threads=0)
         self.graph = ut.Graph(self.csr.indptr_addr, self.csr.indices_addr, self.csr.n_nodes,
                               self.csr.n_edges, keep=self.csr)
         for opt in indptr.split(","):
@@ -1571,7 +1607,8 @@ def main(argv=None):
         raise SystemExit("--warmup must be >= 3")
     if args.gpus < 1:
         raise SystemExit("--gpus must be >= 1")
-    if args.coop == "host" or args.sample != "cpu":
+    if args.coop == "host" or (args.sample != "cpu" and (args.async_sample or args.graph or
+                                                           args.pipeline or args.coop != "off")):
         args.harness = "procs"
     if args.coop == "device" and args.harness == "threads":
         # in-process ranks wait for each other on the device (ut_coop_open_local): one hardware

@@ -236,3 +236,22 @@ def test_gather_host_library_owned_tables(kind, rb):
         t.gather_host(idx_h, out_host=out)
         assert out.numpy().tobytes() == want.tobytes()
         assert t.error_pos() == 11
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("gpus", [1, 2])
+def test_bench_box_harness_gpu_sampling(gpus):
+    """bench.py --sample gpu in the box harness: every GPU worker samples its own minibatch on
+    the GPU from one host CSR and gathers it; the sampled node list and the rows are checked
+    against the oracle on every worker (two workers share the one GPU here)."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(gpus), "--sample", "gpu",
+           "--config", "products", "--steps", "3", "--warmup", "3", "--no-cpu", "--max-lists", "6"]
+    if gpus > 1:
+        cmd.append("--oversubscribe")
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=880, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = json.loads([l for l in p.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == gpus and line["parity_checked"] is True
+    assert line["parity_lists_checked"] == gpus
+    assert line["sampling"]["mode"] == "sync" and line["value"] > 0
+    assert line["harness"].startswith("threads")
