@@ -142,6 +142,22 @@ UT_API int ut_gather_dn(const ut_table* t, const int64_t* idx_dev, const uint64_
                         uint64_t max_n, void* out_dev, ut_stream_t stream);
 
 /*
+ * ut_gather_multi — the box form: one host thread enqueues one gather on each of `count` devices
+ * over the ONE table (every GPU of the box pulling its own minibatch over its own link,
+ * PAPER.md:239-243). For k in [0, count): device devs[k] runs
+ * ut_gather(t, idx_dev[k], n[k], out_dev[k], streams[k]) — idx_dev[k] / out_dev[k] in that
+ * device's memory, streams[k] a stream of that device (NULL: its legacy default stream).
+ * Asynchronous like ut_gather; the calling thread's current device is restored. The first
+ * failing entry stops the call: its error is returned and the entries before it stay enqueued.
+ * A library-owned table (ut_create) is mapped for each device on first use (see ut_create);
+ * a registered table is Portable. Returns UT_OK, UT_EINVAL (count < 1, NULL arrays) or the
+ * failing entry's ut_gather error.
+ */
+UT_API int ut_gather_multi(const ut_table* t, int count, const int* devs,
+                           const int64_t* const* idx_dev, const uint64_t* n,
+                           void* const* out_dev, const ut_stream_t* streams);
+
+/*
  * ut_gather_host — the same gather from and to HOST buffers (the end-to-end form).
  *   idx_host  n int64 row ids in host memory (page-locked for full speed; caller-owned).
  *   out_host  >= n*rb bytes of host memory (caller-owned).

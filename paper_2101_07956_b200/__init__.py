@@ -36,7 +36,8 @@ ABI = ("ut_register", "ut_gather", "ut_gather_host", "ut_release", "ut_error_pos
        "ut_sample_capacity", "ut_graph_launches", "ut_coop_create", "ut_coop_export",
        "ut_coop_open", "ut_coop_dispatch", "ut_coop_fetch", "ut_coop_combine", "ut_coop_gather",
        "ut_coop_get_stats", "ut_coop_error_pos", "ut_coop_owner", "ut_coop_release",
-       "ut_coop_create_partitioned", "ut_coop_partition_ids", "ut_coop_open_local")
+       "ut_coop_create_partitioned", "ut_coop_partition_ids", "ut_coop_open_local",
+       "ut_gather_multi")
 
 UT_COOP_HANDLE_BYTES = 64
 
@@ -105,6 +106,9 @@ def _load():
     L.ut_sample.restype = ctypes.c_int
     L.ut_sample.argtypes = [vp, vp, u64, vp, ctypes.c_int, u64, vp, u64,
                             ctypes.POINTER(ctypes.c_uint64), vp]
+    L.ut_gather_multi.restype = ctypes.c_int
+    L.ut_gather_multi.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(vp),
+                                  ctypes.POINTER(u64), ctypes.POINTER(vp), ctypes.POINTER(vp)]
     L.ut_gather_dn.restype = ctypes.c_int
     L.ut_gather_dn.argtypes = [vp, vp, vp, u64, vp, vp]
     L.ut_sample_async.restype = ctypes.c_int
@@ -260,6 +264,16 @@ def ut_mem_advise(t: int, advice: int, device: int) -> int:
     if rc < 0:
         _check(rc)
     return rc
+
+
+def ut_gather_multi(t: int, devs: list[int], idx_dev: list[int], n: list[int], out_dev: list[int],
+                    streams: list[int] | None = None) -> None:
+    k = len(devs)
+    assert len(idx_dev) == k and len(n) == k and len(out_dev) == k
+    VP = ctypes.c_void_p * k
+    st = VP(*(streams or [0] * k))
+    _check(_lib.ut_gather_multi(t, k, (ctypes.c_int * k)(*devs), VP(*idx_dev),
+                                (ctypes.c_uint64 * k)(*n), VP(*out_dev), st))
 
 
 def ut_gather_dn(t: int, idx_dev: int, n_dev: int, max_n: int, out_dev: int, stream: int = 0) -> None:
@@ -448,6 +462,22 @@ class Table:
         return out
 
     __getitem__ = gather
+
+    def gather_multi(self, idxs, outs=None, streams=None):
+        """The box form (ut_gather_multi): idxs[k] is a CUDA int64 tensor on any device; one
+        call enqueues every device's gather from this thread. Returns the outputs."""
+        import torch
+        if outs is None:
+            outs = [torch.empty((i.numel(), self.row_bytes), dtype=torch.uint8, device=i.device)
+                    for i in idxs]
+        for i, o in zip(idxs, outs):
+            assert i.is_cuda and i.dtype == torch.int64 and i.is_contiguous()
+            assert o.device == i.device and o.numel() * o.element_size() >= i.numel() * self.row_bytes
+        sts = [_stream_handle(s) for s in streams] if streams is not None else \
+              [int(torch.cuda.current_stream(i.device).cuda_stream) for i in idxs]
+        ut_gather_multi(self.handle, [i.device.index for i in idxs], [i.data_ptr() for i in idxs],
+                        [i.numel() for i in idxs], [o.data_ptr() for o in outs], sts)
+        return outs
 
     def gather_dn(self, idx, n_dev, out, stream=None):
         """Gather min(n_dev[0], idx.numel()) rows; the count is read on the device."""

@@ -1198,6 +1198,26 @@ int ut_gather(const ut_table* t, const int64_t* idx_dev, uint64_t n, void* out_d
   return gather_on(t, s, idx_dev, n, out_dev, (cudaStream_t)stream);
 }
 
+int ut_gather_multi(const ut_table* t, int count, const int* devs, const int64_t* const* idx_dev,
+                    const uint64_t* n, void* const* out_dev, const ut_stream_t* streams) {
+  if (!t) return set_err(UT_EINVAL, "table is NULL");
+  if (count < 1 || !devs || !idx_dev || !n || !out_dev)
+    return set_err(UT_EINVAL, "count < 1 or a NULL array");
+  int cur = 0;
+  cudaError_t e = cudaGetDevice(&cur);
+  if (e != cudaSuccess) return cuda_err(e, "cudaGetDevice");
+  int rc = UT_OK;
+  for (int k = 0; k < count && rc == UT_OK; ++k) {
+    if ((e = cudaSetDevice(devs[k])) != cudaSuccess) {
+      rc = cuda_err(e, "cudaSetDevice");
+      break;
+    }
+    rc = ut_gather(t, idx_dev[k], n[k], out_dev[k], streams ? streams[k] : nullptr);
+  }
+  cudaSetDevice(cur);
+  return rc;
+}
+
 int ut_gather_dn(const ut_table* t, const int64_t* idx_dev, const uint64_t* n_dev, uint64_t max_n,
                  void* out_dev, ut_stream_t stream) {
   if (!t || !n_dev) return set_err(UT_EINVAL, "table or n_dev is NULL");

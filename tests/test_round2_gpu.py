@@ -255,3 +255,23 @@ def test_bench_box_harness_gpu_sampling(gpus):
     assert line["parity_lists_checked"] == gpus
     assert line["sampling"]["mode"] == "sync" and line["value"] > 0
     assert line["harness"].startswith("threads")
+
+
+def test_gather_multi_box_form():
+    """ut_gather_multi: one host thread enqueues one gather per entry (device, stream, list);
+    every output equals the oracle's; bad arguments are refused before anything runs."""
+    rows, rb = 50_000, 512
+    with ut.Table.create(rows, rb, "managed") as t:
+        workloads.fill_table(t.host_addr, rows, rb, 901)
+        lists = [workloads.uniform_idx(10_000 + 777 * k, rows, 910 + k) for k in range(3)]
+        lists[2][4] = rows                                  # out of range
+        streams = [torch.cuda.Stream() for _ in lists]
+        idxs = [torch.from_numpy(l).cuda() for l in lists]
+        outs = t.gather_multi(idxs, streams=streams)
+        torch.cuda.synchronize()
+        for l, o in zip(lists, outs):
+            want, _ = oracle.gather(t.host_addr, rows, rb, l)
+            assert o.cpu().numpy().tobytes() == want.tobytes()
+        assert t.error_pos() == 4
+        with pytest.raises(ut.UTError):
+            ut.ut_gather_multi(t.handle, [], [], [], [])
