@@ -918,6 +918,7 @@ class BoxWorker:
             self.table.gather_host(idx_host[k], out_host=out_host, stream=self.stream)
         r = {"e_sec": 0.0, "f_sec": 0.0, "bytes": 0, "h2d": 0, "d2h": 0, "e_ms": [], "f_ms": []}
         start.wait()
+        torch.cuda.nvtx.range_push("e2e")       # ncu --nvtx-include "e2e/" profiles these
         for s in range(args.steps):
             ih = idx_host[(args.warmup + s) % len(idx_host)]
             with torch.cuda.stream(self.stream):
@@ -930,6 +931,7 @@ class BoxWorker:
             r["bytes"] += ih.numel() * rb
             r["h2d"] += ih.numel() * 8
             r["d2h"] += ih.numel() * rb
+        torch.cuda.nvtx.range_pop()
         start.wait()
         for s in range(args.steps):
             ih = idx_host[(args.warmup + s) % len(idx_host)]
