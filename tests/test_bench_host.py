@@ -110,3 +110,23 @@ def test_reference_arm_uses_gpu0_lists_of_the_ut_arm():
     a = bench.config_block(spec, ut_lists, 2, 2101)
     b = bench.config_block(spec, ref_lists, 2, 2101)
     assert a == b and a["seed"] == 2101
+
+
+def test_reference_arm_line_has_the_contract_keys():
+    """`--impl reference` (the oracle on the host cores; no GPU needed) prints one line with the
+    keys the driver reads, the reference-arm extras, and the same config as the ut arm."""
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--config", "tiny", "--steps", "3", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert p.returncode == 0, p.stderr
+    line = _json_line(p.stdout)
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "cpu_baseline", "e2e", "impl"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["higher_is_better"] is True
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] == 1
+    spec = bench.workload_spec("tiny")
+    lists = bench.make_index_lists(spec, 0, 1, 6, 2101, 1)
+    assert line["config"] == bench.config_block(spec, [lists[(3 + s) % 6] for s in range(3)], 1, 2101)

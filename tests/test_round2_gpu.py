@@ -171,6 +171,16 @@ def test_bench_box_harness_tiny():
     assert line["table_memory"].startswith("managed")
     assert line["gpu_launches"] >= 3 and line["value"] > 0
     assert line["step_ms"]["n"] == 3
+    # the driver contract's keys
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "roofline",
+              "e2e", "gpu_launches", "clocks"):
+        assert k in line, k
+    assert set(line["roofline"]) >= {"bound", "achieved", "peak", "unit", "frac", "traffic"}
+    assert set(line["e2e"]) >= {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"}
+    assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
+    assert set(line["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+    assert line["clocks"]["samples_timed"] >= 1
 
 
 @pytest.mark.timeout(600)
