@@ -180,7 +180,7 @@ def test_bench_box_harness_tiny():
     assert set(line["e2e"]) >= {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"}
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
     assert set(line["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
-    assert line["clocks"]["samples_timed"] >= 1
+    assert line["clocks"]["samples"] >= 1
 
 
 @pytest.mark.timeout(600)
