@@ -285,3 +285,18 @@ def test_gather_multi_box_form():
         assert t.error_pos() == 4
         with pytest.raises(ut.UTError):
             ut.ut_gather_multi(t.handle, [], [], [], [])
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("extra", [["--harness", "procs", "--config", "tiny"],
+                                   ["--sample", "gpu", "--graph", "--async-sample",
+                                    "--config", "products", "--graph-indptr", "hbm"]])
+def test_bench_procs_harness(extra):
+    """The one-process-per-GPU form still runs end to end at N = 1 (plain, and GPU sampling
+    replayed from a CUDA graph, which only this form has)."""
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3",
+                        "--warmup", "3", "--no-cpu", "--max-lists", "6", *extra],
+                       capture_output=True, text=True, timeout=880, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = json.loads([l for l in p.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 1 and line["parity_checked"] is True and line["value"] > 0
