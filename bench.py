@@ -887,6 +887,12 @@ class BoxWorker:
         start.wait()
         torch.cuda.nvtx.range_push("timed")    # ncu --nvtx-include "timed/" profiles these
         t0 = time.perf_counter()
+        if self.sampler is not None and args.pipeline:
+            # sample minibatch k+1 (its own stream) while minibatch k is gathered; one timed
+            # region for the K steps (every step writes > L2: no flush, stated in the line)
+            nbytes, ms = self.sampler.pipelined(args.warmup, args.steps, self.table, self.out)
+            torch.cuda.nvtx.range_pop()
+            return {"bytes": nbytes, "ms": [ms], "wall_s": time.perf_counter() - t0}
         evs, nbytes = [], 0
         for s in range(args.steps):
             with torch.cuda.stream(self.stream):
@@ -1208,6 +1214,8 @@ def run_box(args, spec, dist=None):
         py_base = cpu_staged_baseline(torch, hb.addr, spec, lists[0], args)
 
     cfg = config_block(spec, timed_lists, N, seed)
+    if samplers is not None and args.pipeline:
+        cfg["l2"] = "not flushed: sampling k+1 overlaps gathering k in one timed region (each step writes > L2)"
     sect_ratio = (cfg["sector_floor_mb_per_step"] / cfg["mb_per_step_per_gpu"]
                   if cfg.get("mb_per_step_per_gpu") else None)
     link_g = statistics.mean(link_solo)
@@ -1222,7 +1230,9 @@ def run_box(args, spec, dist=None):
         "harness": "threads: one process drives all GPUs (one host thread each) over one table"
                    + (f" (--oversubscribe: {N} workers on {ndev} device(s), a harness test, not "
                       f"a scaling measurement)" if args.oversubscribe and ndev < N else ""),
-        "step_ms": step_stats(all_ms),
+        "step_ms": (step_stats(all_ms) if not (samplers is not None and args.pipeline) else
+                    {"note": "--pipeline: one timed region per GPU for all K steps",
+                     "region_ms": [round(m, 4) for m in all_ms]}),
         "per_gpu_gbs": [round(x, 3) for x in per_gpu],
         "transferred_gbs_sector_floor": round(value * sect_ratio, 3) if sect_ratio else None,
         "line_requests_per_s": (round(cfg["line_requests_per_step"] * N / (max(dev_ms) / args.steps / 1e3))
@@ -1610,7 +1620,7 @@ def main(argv=None):
     if args.gpus < 1:
         raise SystemExit("--gpus must be >= 1")
     if args.coop == "host" or (args.sample != "cpu" and (args.async_sample or args.graph or
-                                                           args.pipeline or args.coop != "off")):
+                                                           args.coop != "off")):
         args.harness = "procs"
     if args.coop == "device" and args.harness == "threads":
         # in-process ranks wait for each other on the device (ut_coop_open_local): one hardware

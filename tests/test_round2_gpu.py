@@ -300,3 +300,16 @@ def test_bench_procs_harness(extra):
     assert p.returncode == 0, p.stderr[-3000:]
     line = json.loads([l for l in p.stdout.splitlines() if l.startswith("{")][-1])
     assert line["n_gpus"] == 1 and line["parity_checked"] is True and line["value"] > 0
+
+
+@pytest.mark.timeout(900)
+def test_bench_box_harness_gpu_sampling_pipelined():
+    """--sample gpu --pipeline in the box harness (sampling of k+1 overlaps the gather of k)."""
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--sample", "gpu",
+                        "--pipeline", "--graph-indptr", "hbm,indices=hbm", "--config", "products",
+                        "--steps", "4", "--warmup", "3", "--no-cpu", "--max-lists", "7"],
+                       capture_output=True, text=True, timeout=880, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = json.loads([l for l in p.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["harness"].startswith("threads") and line["parity_checked"] is True
+    assert line["value"] > 0 and "region_ms" in line["step_ms"]
