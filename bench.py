@@ -1044,7 +1044,7 @@ def run_box(args, spec, dist=None):
     if args.sample == "gpu":
         # GPU-side neighbour sampling on every GPU from ONE host CSR: each worker
         # samples its own roots' minibatch, then gathers it (sync mode: one count read per step)
-        assert args.coop == "off", "--sample gpu with --coop: use --harness procs"
+        assert not (args.pipeline and args.coop != "off"), "--pipeline with --coop: not supported"
         csr = workloads.CSRGraph(spec["rows"], spec["edges"], seed=seed, threads=0)
 
         def mk_sampler(g):
@@ -1065,6 +1065,8 @@ def run_box(args, spec, dist=None):
         # each row requested by several GPUs in a step is fetched from the host table once, by
         # its owner, and exchanged over NVLink peer memory
         max_n = max(l.size for ls in lists for l in ls)
+        if samplers is not None:          # a sampled minibatch may reach the sampler's bound
+            max_n = max(smp.capacity() for smp in samplers)
 
         def mk(g):
             torch.cuda.set_device(dev_of(g))
@@ -1073,6 +1075,8 @@ def run_box(args, spec, dist=None):
         run_threads(N, lambda g: (torch.cuda.set_device(dev_of(g)), coops[g].open_local(coops)))
         for g in range(N):
             workers[g].coop = coops[g]
+            if samplers is not None:      # the sampled rows go through the cooperative gather
+                samplers[g].gather_fn = (lambda c: lambda nodes, o: c.gather(nodes, out=o))(coops[g])
 
     # roofline denominators, measured now: each GPU's link alone, then all at once
     ndevs = len({dev_of(g) for g in range(N)})
@@ -1619,8 +1623,7 @@ def main(argv=None):
         raise SystemExit("--warmup must be >= 3")
     if args.gpus < 1:
         raise SystemExit("--gpus must be >= 1")
-    if args.coop == "host" or (args.sample != "cpu" and (args.async_sample or args.graph or
-                                                           args.coop != "off")):
+    if args.coop == "host" or (args.sample != "cpu" and (args.async_sample or args.graph)):
         args.harness = "procs"
     if args.coop == "device" and args.harness == "threads":
         # in-process ranks wait for each other on the device (ut_coop_open_local): one hardware

@@ -313,3 +313,19 @@ def test_bench_box_harness_gpu_sampling_pipelined():
     line = json.loads([l for l in p.stdout.splitlines() if l.startswith("{")][-1])
     assert line["harness"].startswith("threads") and line["parity_checked"] is True
     assert line["value"] > 0 and "region_ms" in line["step_ms"]
+
+
+@pytest.mark.timeout(900)
+def test_bench_box_harness_gpu_sampling_coop():
+    """--sample gpu --coop device in the box harness: each worker samples on the GPU and gathers
+    its sampled rows through the in-process cooperative gather (two workers on this one GPU)."""
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--oversubscribe", "--sample", "gpu", "--coop", "device",
+                        "--graph-indptr", "hbm,indices=hbm", "--config", "products", "--steps", "3",
+                        "--warmup", "3", "--no-cpu", "--max-lists", "6"],
+                       capture_output=True, text=True, timeout=880, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = json.loads([l for l in p.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["parity_checked"] is True
+    assert line["coop"] is not None and line["coop"]["host_bytes_fraction"] < 1.0
+    assert line["sampling"]["mode"] == "sync"
