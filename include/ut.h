@@ -167,7 +167,9 @@ UT_API int ut_gather_multi(const ut_table* t, int count, const int* devs,
  * chunks into library-owned device
  * scratch and copied back by the copy engine on a second stream, overlapping the two link
  * directions (UT_HOST_PIPELINE=1 forces this path). Device scratch is owned by the table and
- * grown on demand. Synchronous: returns after out_host holds the result, on `stream`.
+ * grown on demand (x1.5 in whole MiB, since a reallocation synchronises the device).
+ * Synchronous: returns after out_host holds the result, on `stream`. Calls on different devices
+ * run concurrently; calls on the same device serialise (they share that device's scratch).
  * Out-of-range handling as ut_gather. Returns UT_OK, UT_EINVAL, UT_ENOMEM or UT_ECUDA.
  */
 UT_API int ut_gather_host(const ut_table* t, const int64_t* idx_host, uint64_t n, void* out_host,
