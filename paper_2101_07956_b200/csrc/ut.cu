@@ -335,6 +335,7 @@ struct ut_table {
   int runs = -1;                        // run merge: -1 auto, 0 off, 1 on ("runs=...")
   int stage = -1;                       // host-output tile staging: -1 auto (= off), 0 off, 1 on ("stage=...")
   int share = -1;                       // neighbour line sharing: -1 auto, 0 off, 1 on ("share=...")
+  int exact = -1;                       // reorder: exact row order inside each bucket ("exact=...")
   std::mutex mu;
   DevState dev[kMaxDev];
 };
@@ -625,6 +626,7 @@ int bucket_shift(uint64_t table_bytes, uint64_t rb) {
 }
 
 bool want_runs(const ut_table* t, const Plan& p, uint64_t n);
+bool want_exact(const ut_table* t, uint64_t n, uint32_t nb);
 template <typename F>
 cudaError_t timed(const ut_table* t, DevState* s, cudaStream_t st, F&& fn);
 
@@ -761,6 +763,10 @@ int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n
     ut::k_bucket_scan<<<1, 1024, hsm, st>>>(cnt, nb);
     ut::k_bucket_scatter<<<(int)blocks, 512, hsm, st>>>(c, shift, nb, per_block, cnt, perm);
     s->launches += 3;
+    if (want_exact(t, cnt_n, nb)) {     // cnt[] now holds the bucket ends
+      ut::k_bucket_sort<<<(int)((nb + 255) / 256), 256, 0, st>>>(c, cnt, nb, perm);
+      s->launches += 1;
+    }
     e = cudaGetLastError();
     if (e == cudaSuccess) e = timed_launch<true>(t, s, p, st, c, host_out);
     cudaError_t e2 = cudaFreeAsync(scratch, st);
@@ -966,6 +972,18 @@ bool want_reorder(const ut_table* t, uint64_t n) {
   const bool partial = t->rb > 128 && t->rb < 1024 && (t->rb & 127) != 0;
   if (t->alloc_kind == UT_ALLOC_MANAGED) return small_rows || (partial && t->bytes > (1ull << 30));
   return t->bytes > (1ull << 30) || small_rows;
+}
+
+// Exact row order inside each reorder bucket ("exact=on"; k_bucket_sort, one thread per bucket,
+// insertion sort of buckets up to 256 items): consecutive work items then touch ascending
+// addresses, not just the same 2-MiB region. A/B knob; "auto" decides by measurement
+// (DESIGN.md §6).
+bool want_exact(const ut_table* t, uint64_t n, uint32_t nb) {
+  if (t->exact == 0) return false;
+  if (t->exact == 1) return true;
+  (void)n;
+  (void)nb;
+  return false;
 }
 
 }  // namespace
@@ -1444,6 +1462,14 @@ int ut_set_plan(ut_table* t, const char* name) {
     else if (!strcmp(v, "on")) t->share = 1;
     else if (!strcmp(v, "off")) t->share = 0;
     else return set_err(UT_EINVAL, "share must be auto|on|off, got '%s'", v);
+    return UT_OK;
+  }
+  if (!strncmp(name, "exact=", 6)) {
+    const char* v = name + 6;
+    if (!strcmp(v, "auto")) t->exact = -1;
+    else if (!strcmp(v, "on")) t->exact = 1;
+    else if (!strcmp(v, "off")) t->exact = 0;
+    else return set_err(UT_EINVAL, "exact must be auto|on|off, got '%s'", v);
     return UT_OK;
   }
   if (!strncmp(name, "stage=", 6)) {
