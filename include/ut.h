@@ -224,6 +224,8 @@ UT_API const char* ut_plan_probe(uint64_t base, uint64_t rows, uint64_t row_byte
  * two share, so the line is requested once; auto = on for gathers of >= 64K rows
  * that select >= 1/16 of the table (host-known row counts only). Costs a hash of the selection,
  * 8 B x 2^ceil(log2 2n), of stream-ordered scratch per gather (O(n), independent of the table).
+ * "exact=on|off|auto" (auto = off): with the reorder, sort the work items of each 2-MiB bucket
+ * exactly by row id (an A/B knob: measured no gain).
  * "stage=on|off|auto" (auto = off): ut_gather_host's direct path gathers tiles of consecutive
  * output rows into shared memory and writes each tile's span with whole-line stores (k_staged;
  * an A/B knob — measured no gain).

@@ -28,7 +28,8 @@ for rb, off in [(4, 0), (8, 8), (68, 3), (400, 0), (400, 4), (144, 0), (2052, 1)
             except ut.UTError:
                 continue
             for reorder in ["reorder=off,runs=off,share=off", "reorder=on,runs=off,share=off",
-                            "reorder=off,runs=on,share=off", "reorder=off,runs=off,share=on"]:
+                            "reorder=on,runs=off,share=off,exact=on",
+                            "reorder=off,runs=on,share=off,exact=off", "reorder=off,runs=off,share=on"]:
                 for m in reorder.split(","):
                     t.set_plan(m)
                 buf = torch.zeros(700 * rb + 16, dtype=torch.uint8, device="cuda")
@@ -37,7 +38,7 @@ for rb, off in [(4, 0), (8, 8), (68, 3), (400, 0), (400, 4), (144, 0), (2052, 1)
                 if got.tobytes() != want.tobytes():
                     bad += 1
                     print("MISMATCH", rb, plan, reorder)
-        for m in ["auto", "reorder=auto", "runs=auto", "share=auto"]:
+        for m in ["auto", "reorder=auto", "runs=auto", "share=auto", "exact=auto"]:
             t.set_plan(m)
         o = t.gather_host(torch.from_numpy(idx).pin_memory())
         bad += o.numpy().tobytes() != want.tobytes()

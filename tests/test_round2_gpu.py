@@ -329,3 +329,25 @@ def test_bench_box_harness_gpu_sampling_coop():
     assert line["n_gpus"] == 2 and line["parity_checked"] is True
     assert line["coop"] is not None and line["coop"]["host_bytes_fraction"] < 1.0
     assert line["sampling"]["mode"] == "sync"
+
+
+@pytest.mark.parametrize("rb", [68, 512, 2408])
+def test_reorder_exact_order(rb):
+    """reorder=on with exact in-bucket order (exact=on): same bytes as the oracle, including
+    duplicates, out-of-range ids and a misaligned output."""
+    rows = (1_200 << 20) // rb                    # beyond 1 GiB: 2-MiB buckets
+    hb = workloads.HostBuffer(rows * rb)
+    workloads.fill_table(hb.addr, rows, rb, 1001, threads=0)
+    idx = workloads.uniform_idx(200_000, rows, 1002)
+    idx[::997] = idx[3]
+    idx[11] = rows
+    want, bad = oracle.gather(hb.addr, rows, rb, idx)
+    with ut.Table(hb.addr, rows, rb) as t:
+        t.set_plan("reorder=on")
+        t.set_plan("exact=on")
+        for off in (0, 4):
+            buf = torch.full((idx.size * rb + off,), 0xAB, dtype=torch.uint8, device="cuda")
+            t.gather(torch.from_numpy(idx).cuda(), out=buf[off:])
+            assert buf[off:].cpu().numpy().tobytes() == want.tobytes()
+            assert t.error_pos() == bad == 11
+    hb.close()
