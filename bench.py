@@ -322,7 +322,7 @@ def cpu_oracle_rate(table_addr: int, spec: dict, lists: list[np.ndarray], budget
         done_bytes += l.size * rb
         done_lists += 1
         el = time.perf_counter() - t0
-        if el >= budget_s or done_lists >= 4 * len(lists):
+        if el >= budget_s or done_lists >= 64 * len(lists):
             break
     return done_bytes / el / 1e9, done_lists, el
 
@@ -808,8 +808,23 @@ def box_table(spec: dict, args, ut):
         import paper_2101_07956_b200 as _ut
         return _ut.Table(hb.addr, rows, rb), hb, kind
     table = ut.Table.create(rows, rb, kind)
+    owned = _Owned(table.host_addr)
+    # the box's one table NUMA-interleaved (2-MiB stripes placed by SetPreferredLocation
+    # = host NUMA node, before the fill first-touches them); a no-op policy on one-node boxes
+    nodes = workloads.numa_nodes()
+    if kind == "managed" and (args.numa == "interleave" or (args.numa == "auto" and nodes > 1)):
+        t0 = time.perf_counter()
+        try:
+            table.numa_interleave(max(nodes, 1))
+            owned.numa = {"policy": f"interleave over {max(nodes, 1)} node(s), 2-MiB stripes "
+                                    "(ut_numa_interleave)", "advise_s": round(time.perf_counter() - t0, 3)}
+        except ut.UTError as e:
+            owned.numa = {"policy": "first touch by the fill threads (interleave requested, not "
+                                    f"available: {str(e)[:160]})"}
+    else:
+        owned.numa = {"policy": "first touch by the fill threads" + ("" if nodes > 1 else " (one NUMA node)")}
     workloads.fill_table(table.host_addr, rows, rb, args.seed, threads=threads)
-    return table, _Owned(table.host_addr), kind
+    return table, owned, kind
 
 
 class BoxWorker:
@@ -1254,6 +1269,9 @@ def run_box(args, spec, dist=None):
         "plan": plan_label,
         "table_memory": kind + (" (cudaMallocManaged + SetPreferredLocation=CPU + SetAccessedBy "
                                 "every GPU: one copy for the box)" if kind == "managed" else ""),
+        "numa": {"nodes": workloads.numa_nodes(),
+                 **(hb.numa if isinstance(getattr(hb, "numa", None), dict) else
+                    {"policy": "mbind interleave" if getattr(hb, "numa", 0) > 1 else "first touch"})},
         "roofline": {"bound": "pcie_h2d",
                      "achieved": round(achieved, 3) if achieved is not None else None,
                      "peak": round(link_g, 3), "unit": "GB/s",
@@ -1601,6 +1619,9 @@ def main(argv=None):
     ap.add_argument("--alloc", default="auto", choices=["auto", "register", "pinned", "managed", "vmm"],
                     help="table memory: auto = managed (the paper's unified tensor) in the threads "
                          "harness; in procs: managed for one rank and a table > 1 GiB, else register")
+    ap.add_argument("--numa", default="auto", choices=["auto", "interleave", "off"],
+                    help="threads harness, managed table: stripe its pages over the host NUMA nodes "
+                         "(auto: when the box has more than one node)")
     ap.add_argument("--sample", default="cpu", choices=["cpu", "gpu"],
                     help="cpu: index lists sampled before timing (default, the paper's split); "
                          "gpu: ut_sample inside every timed step (SURVEY NEXT-2; implies --harness procs)")

@@ -253,6 +253,28 @@ UT_API int ut_set_plan(ut_table* t, const char* name);
  */
 UT_API int ut_mem_advise(const ut_table* t, int advice, int device);
 
+/*
+ * ut_numa_interleave — stripe a managed table's host pages round-robin over host NUMA nodes
+ * 0..nodes-1 (the box's one shared table is "NUMA-interleaved by default", so on a
+ * two-socket box each socket's GPUs read half their rows from local DRAM and neither socket's
+ * memory carries the whole box's gather traffic). It is the paper's memAdvise interface (Table 2,
+ * PAPER.md:413-416) with CUDA's host-NUMA location: stripe k of `chunk_bytes` gets
+ * cudaMemAdvise(SetPreferredLocation, {HostNuma, k mod nodes}); SetAccessedBy is unchanged, so
+ * GPUs keep reading the pages in place over the link. The advice places pages when they are first
+ * populated: call it between ut_create(src = NULL) and the first write of the table.
+ *   t            a UT_ALLOC_MANAGED table.
+ *   nodes        >= 1 host NUMA nodes, ids 0..nodes-1 (nodes == 1: the whole table on node 0).
+ *   chunk_bytes  stripe size, rounded up to a multiple of 2 MiB (the managed-memory block);
+ *                0 = 2 MiB.
+ * The placement is read back (cudaMemRangeGetAttribute) on the first stripe of every node.
+ * Returns UT_OK, UT_EINVAL (NULL table, nodes < 1), UT_ENOTSUP (not a managed table, or the
+ * driver accepted the advice without applying it — measured on this pool's virtualised boxes) or
+ * UT_ECUDA (the runtime refused the advice, e.g. a node id the host does not have). On either
+ * error the whole table is advised back to SetPreferredLocation = CPU, the state ut_create left
+ * it in.
+ */
+UT_API int ut_numa_interleave(const ut_table* t, int nodes, uint64_t chunk_bytes);
+
 /* ---- GPU-side neighbour sampling over a host-resident CSR graph -------------
  * The step before the gather that the paper leaves on the CPU. The CSR stays in
  * host memory (pinned in place like a feature table) and GPU threads read it over the link. */

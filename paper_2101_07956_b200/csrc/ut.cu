@@ -1561,6 +1561,56 @@ int ut_mem_advise(const ut_table* t, int advice, int device) {
   return (int)e;
 }
 
+int ut_numa_interleave(const ut_table* t, int nodes, uint64_t chunk_bytes) {
+  if (!t) return set_err(UT_EINVAL, "table is NULL");
+  if (nodes < 1) return set_err(UT_EINVAL, "nodes must be >= 1 (got %d)", nodes);
+  if (t->alloc_kind != UT_ALLOC_MANAGED)
+    return set_err(UT_ENOTSUP, "NUMA striping needs a managed table (ut_create UT_ALLOC_MANAGED)");
+  constexpr uint64_t kBlock = 2ull << 20;
+  const uint64_t chunk = chunk_bytes == 0 ? kBlock : (chunk_bytes + kBlock - 1) / kBlock * kBlock;
+  auto restore = [&] {
+    cudaMemLocation cpu{};
+    cpu.type = cudaMemLocationTypeHost;
+    cpu.id = 0;
+    cudaMemAdvise(t->host, t->bytes, cudaMemAdviseSetPreferredLocation, cpu);
+    cudaGetLastError();
+  };
+  uint64_t k = 0;
+  for (uint64_t off = 0; off < t->bytes; off += chunk, ++k) {
+    cudaMemLocation loc{};
+    loc.type = cudaMemLocationTypeHostNuma;
+    loc.id = (int)(k % (uint64_t)nodes);
+    const cudaError_t e = cudaMemAdvise(t->host + off, std::min(chunk, t->bytes - off),
+                                        cudaMemAdviseSetPreferredLocation, loc);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      restore();
+      return cuda_err(e, "cudaMemAdvise(SetPreferredLocation = host NUMA node)");
+    }
+  }
+  // Read the advice back: a driver can accept a host-NUMA location and not apply it (measured on
+  // this pool's virtualised GPU boxes: cudaSuccess, then no preferred location at all), and a
+  // table whose placement silently stayed elsewhere must not be reported as striped.
+  for (uint64_t j = 0; j < std::min<uint64_t>(k, (uint64_t)nodes); ++j) {
+    const uint64_t off = j * chunk;
+    int typ = -1, id = -1;
+    const uint64_t len = std::min<uint64_t>(4096, t->bytes - off);
+    if (cudaMemRangeGetAttribute(&typ, 4, cudaMemRangeAttributePreferredLocationType,
+                                 t->host + off, len) != cudaSuccess ||
+        cudaMemRangeGetAttribute(&id, 4, cudaMemRangeAttributePreferredLocationId, t->host + off,
+                                 len) != cudaSuccess ||
+        typ != (int)cudaMemLocationTypeHostNuma || id != (int)(j % (uint64_t)nodes)) {
+      cudaGetLastError();
+      restore();
+      return set_err(UT_ENOTSUP, "the driver accepted SetPreferredLocation = host NUMA node %d but "
+                     "reports location type %d id %d for stripe %llu: host-NUMA placement is not "
+                     "available here (the table keeps SetPreferredLocation = CPU)",
+                     (int)(j % (uint64_t)nodes), typ, id, (unsigned long long)j);
+    }
+  }
+  return UT_OK;
+}
+
 int ut_table_get_info(const ut_table* t, ut_table_info* info) {
   if (!t || !info) return set_err(UT_EINVAL, "NULL argument");
   info->rows = t->rows;

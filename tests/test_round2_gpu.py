@@ -351,3 +351,58 @@ def test_reorder_exact_order(rb):
             assert buf[off:].cpu().numpy().tobytes() == want.tobytes()
             assert t.error_pos() == bad == 11
     hb.close()
+
+
+def _preferred(addr: int, nbytes: int):
+    """(location type, id) of a managed range's SetPreferredLocation: cudaMemRangeGetAttribute
+    (PreferredLocationType = 5, PreferredLocationId = 6; driver_types.h) through torch's libcudart."""
+    import ctypes
+    lib = os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "cuda_runtime", "lib",
+                       "libcudart.so.12")
+    rt = ctypes.CDLL(lib if os.path.exists(lib) else "libcudart.so.12")
+    f = rt.cudaMemRangeGetAttribute
+    f.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t]
+    typ, loc = ctypes.c_int(-1), ctypes.c_int(-1)
+    assert f(ctypes.byref(typ), 4, 5, addr, nbytes) == 0
+    assert f(ctypes.byref(loc), 4, 6, addr, nbytes) == 0
+    names = {2: "cudaMemLocationTypeHost", 3: "cudaMemLocationTypeHostNuma"}
+    return names.get(typ.value, typ.value), loc.value
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("chunk", [0, 5 << 20])
+def test_numa_interleave_managed_table(chunk):
+    """ut_numa_interleave stripes a managed table over host NUMA nodes before it is
+    filled; the gather still reads every row in place (bytes vs the oracle). Node 0 is the one
+    node every box has; the argument and kind checks are exercised too."""
+    rows, rb = 50_000, 512          # 25.6 MB: several 2-MiB stripes and a partial last one
+    with ut.Table.create(rows, rb, "managed") as t:
+        assert _preferred(t.host_addr + (rows * rb) // 2, 4096)[0] == "cudaMemLocationTypeHost"
+        try:
+            t.numa_interleave(1, chunk)
+            applied = True
+        except ut.UTError as e:
+            # a driver that accepts the advice without applying it (this pool's virtualised
+            # boxes) must be reported, and the table left as ut_create made it
+            assert e.code == ut.UT_ENOTSUP and "not available" in str(e), e
+            applied = False
+        want = ("cudaMemLocationTypeHostNuma", 0) if applied else ("cudaMemLocationTypeHost", -1)
+        for off in range(0, rows * rb, 1 << 20):
+            got = _preferred(t.host_addr + off, 4096)
+            assert got == want or (not applied and got[0] == want[0]), (off, got)
+        with pytest.raises(ut.UTError) as ei:       # a node this host does not have
+            t.numa_interleave(1 << 20)
+        assert ei.value.code in (ut.UT_ECUDA, ut.UT_ENOTSUP)
+        assert _preferred(t.host_addr, 4096)[0] == "cudaMemLocationTypeHost"
+        workloads.fill_table(t.host_addr, rows, rb, seed=301)
+        idx = workloads.uniform_idx(20_000, rows, 302)
+        want, _ = oracle.gather(t.host_addr, rows, rb, idx)
+        got = t[torch.from_numpy(idx).cuda()].cpu().numpy().reshape(-1)
+        assert got.tobytes() == want.tobytes()
+        with pytest.raises(ut.UTError) as ei:
+            t.numa_interleave(0)
+        assert ei.value.code == ut.UT_EINVAL
+    with ut.Table.create(1024, 64, "pinned") as t:
+        with pytest.raises(ut.UTError) as ei:
+            t.numa_interleave(1)
+        assert ei.value.code == ut.UT_ENOTSUP
