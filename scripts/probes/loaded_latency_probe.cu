@@ -94,10 +94,22 @@ __global__ void __launch_bounds__(256) k_load(const uint8_t* __restrict__ table,
   if ((acc.x & 0xFFFFF) == 0x12345) sink[0] = acc;
 }
 
+// Sequential 16-B stores into mapped host memory (the write half of a host->host gather).
+__global__ void k_store(uint4* __restrict__ a, uint64_t n16, const volatile int* go) {
+  if (go) {
+    const uint64_t ts = gtime();
+    while (*go == 0)
+      if (gtime() - ts > 2000000000ull) break;
+  }
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * blockDim.x)
+    a[i] = make_uint4((uint32_t)i, 1, 2, 3);
+}
+
 int main(int argc, char** argv) {
   const double gib = argc > 1 ? atof(argv[1]) : 4.0;
   const int only_load = argc > 3 ? atoi(argv[3]) : 0;   // 1: the load kernel alone (no chase)
   const int skip = argc > 4 ? atoi(argv[4]) : 0;        // bit 0: no ring writes, bit 1: no unloaded chase
+  const int duplex = argc > 5 ? atoi(argv[5]) : 0;      // 1: only the read load beside host stores
   const uint64_t bytes = (uint64_t)(gib * (1ull << 30)) & ~4095ull;
   CK(cudaSetDevice(0));
   uint8_t* table = nullptr;
@@ -158,6 +170,51 @@ int main(int argc, char** argv) {
     printf("{\"probe\": \"loaded_latency\", \"window_mib\": %llu, \"load\": \"none\", \"latency_ns\": %.1f}\n",
            (unsigned long long)(win >> 20), (double)res[0] / hops);
     fflush(stdout);
+    }
+    if (duplex) {
+      // saturated random-line reads (P = 128) with a concurrent store stream into pinned host
+      // memory of a chosen width: what the host->host gather's writes do to its reads
+      static uint8_t* hw = nullptr;
+      const uint64_t wbytes = 1ull << 30;
+      if (!hw) CK(cudaHostAlloc(&hw, wbytes, cudaHostAllocMapped));
+      uint4* hwd;
+      CK(cudaHostGetDevicePointer((void**)&hwd, hw, 0));
+      cudaStream_t s3;
+      CK(cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking));
+      cudaEvent_t c, d;
+      cudaEventCreate(&c);
+      cudaEventCreate(&d);
+      // warm-up: the GPU's first touch of the window and of the store buffer (slow first
+      // mappings on this pool's virtualised boxes) stays out of the measured runs
+      k_load<1><<<1184, 256, 0, s2>>>(table, dl, n, 128, nullptr, sink);
+      k_store<<<148, 256, 0, s3>>>(hwd, wbytes / 16, nullptr);
+      CK(cudaDeviceSynchronize());
+      for (int sb : {0, 8, 18, 37, 74, 148, 296}) {
+        CK(cudaMemset(go, 0, 4));
+        CK(cudaDeviceSynchronize());
+        k_chase<true><<<1, 32, 0, s1>>>(table, ids[sb % ring], hops, go, res);
+        if (sb) {
+          cudaEventRecord(c, s3);
+          k_store<<<sb, 256, 0, s3>>>(hwd, wbytes / 16, go);
+          cudaEventRecord(d, s3);
+        }
+        cudaEventRecord(a, s2);
+        k_load<1><<<1184, 256, 0, s2>>>(table, dl, n, 128, go, sink);
+        cudaEventRecord(b, s2);
+        CK(cudaDeviceSynchronize());
+        float ms = 0, wms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        if (sb) cudaEventElapsedTime(&wms, c, d);
+        const double rate = n / (ms / 1e3);
+        const double lat = (double)res[0] / hops;
+        printf("{\"probe\": \"duplex\", \"window_mib\": %llu, \"store_blocks\": %d, \"read_ms\": %.3f, "
+               "\"read_requests_per_s_M\": %.1f, \"read_gbs\": %.2f, \"store_ms\": %.3f, \"store_gbs\": %.2f, "
+               "\"latency_ns\": %.1f, \"in_flight_little\": %.0f}\n",
+               (unsigned long long)(win >> 20), sb, ms, rate / 1e6, rate * 128 / 1e9, wms,
+               sb ? wbytes / (wms / 1e3) / 1e9 : 0.0, lat, rate * lat * 1e-9);
+        fflush(stdout);
+      }
+      continue;
     }
     // chase: 0 = none (the load alone), 1 = ld.global.cv, 2 = ld.global.nc
     for (int chase : {0, 1, 2})
