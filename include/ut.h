@@ -133,6 +133,18 @@ UT_API int ut_gather(const ut_table* t, const int64_t* idx_dev, uint64_t n, void
               ut_stream_t stream);
 
 /*
+ * ut_gather_i32 — ut_gather with 32-bit row ids (a GPU index tensor of dtype int32, which
+ * PyTorch's indexing also accepts; reading R2 keeps int64 as the native form because
+ * the 4-B sweep table has 2^32 rows). The ids are sign-extended into stream-ordered library
+ * scratch (12 B of HBM traffic per row, one small launch) and gathered exactly as ut_gather
+ * does: the same bytes, the same out-of-range rule (a negative id is out of range; its row is
+ * zero-filled and its position recorded for ut_error_pos). Arguments, layout, ownership and
+ * errors as ut_gather, plus UT_ENOMEM when the scratch cannot be allocated.
+ */
+UT_API int ut_gather_i32(const ut_table* t, const int32_t* idx_dev, uint64_t n, void* out_dev,
+                         ut_stream_t stream);
+
+/*
  * ut_gather_dn — ut_gather whose row count lives in device memory: gathers
  * min(*n_dev, max_n) rows, read by the kernels themselves, so a device-side producer of the index
  * list (ut_sample_async) and this gather need no host synchronisation between them and can be

@@ -37,7 +37,7 @@ ABI = ("ut_register", "ut_gather", "ut_gather_host", "ut_release", "ut_error_pos
        "ut_coop_open", "ut_coop_dispatch", "ut_coop_fetch", "ut_coop_combine", "ut_coop_gather",
        "ut_coop_get_stats", "ut_coop_error_pos", "ut_coop_owner", "ut_coop_release",
        "ut_coop_create_partitioned", "ut_coop_partition_ids", "ut_coop_open_local",
-       "ut_gather_multi", "ut_numa_interleave")
+       "ut_gather_multi", "ut_numa_interleave", "ut_gather_i32")
 
 UT_COOP_HANDLE_BYTES = 64
 
@@ -109,6 +109,8 @@ def _load():
     L.ut_gather_multi.restype = ctypes.c_int
     L.ut_gather_multi.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(vp),
                                   ctypes.POINTER(u64), ctypes.POINTER(vp), ctypes.POINTER(vp)]
+    L.ut_gather_i32.restype = ctypes.c_int
+    L.ut_gather_i32.argtypes = [vp, vp, u64, vp, vp]
     L.ut_gather_dn.restype = ctypes.c_int
     L.ut_gather_dn.argtypes = [vp, vp, vp, u64, vp, vp]
     L.ut_sample_async.restype = ctypes.c_int
@@ -194,6 +196,10 @@ def ut_create(src: int, rows: int, row_bytes: int, kind: int) -> tuple[int, int]
 
 def ut_gather(t: int, idx_dev: int, n: int, out_dev: int, stream: int = 0) -> None:
     _check(_lib.ut_gather(t, idx_dev, n, out_dev, stream))
+
+
+def ut_gather_i32(t: int, idx_dev: int, n: int, out_dev: int, stream: int = 0) -> None:
+    _check(_lib.ut_gather_i32(t, idx_dev, n, out_dev, stream))
 
 
 def ut_gather_host(t: int, idx_host: int, n: int, out_host: int, stream: int = 0) -> None:
@@ -460,16 +466,18 @@ class Table:
         return ut_get_stats(self.handle, reset)
 
     def gather(self, idx, out=None, stream=None):
-        """out[i] = row idx[i] (uint8 [n, row_bytes] CUDA tensor); idx: CUDA int64 tensor."""
+        """out[i] = row idx[i] (uint8 [n, row_bytes] CUDA tensor); idx: CUDA int64 (or int32)
+        tensor."""
         import torch
-        assert idx.is_cuda and idx.dtype == torch.int64 and idx.is_contiguous()
+        assert idx.is_cuda and idx.dtype in (torch.int64, torch.int32) and idx.is_contiguous()
         n = idx.numel()
         if out is None:
             out = torch.empty((n, self.row_bytes), dtype=torch.uint8, device=idx.device)
         else:
             assert out.is_cuda and out.is_contiguous()
             assert out.numel() * out.element_size() >= n * self.row_bytes
-        ut_gather(self.handle, idx.data_ptr(), n, out.data_ptr(), _stream_handle(stream))
+        go = ut_gather if idx.dtype == torch.int64 else ut_gather_i32
+        go(self.handle, idx.data_ptr(), n, out.data_ptr(), _stream_handle(stream))
         return out
 
     __getitem__ = gather

@@ -1216,6 +1216,32 @@ int ut_gather(const ut_table* t, const int64_t* idx_dev, uint64_t n, void* out_d
   return gather_on(t, s, idx_dev, n, out_dev, (cudaStream_t)stream);
 }
 
+int ut_gather_i32(const ut_table* t, const int32_t* idx_dev, uint64_t n, void* out_dev, ut_stream_t stream) {
+  if (!t) return set_err(UT_EINVAL, "table is NULL");
+  if (n == 0) return UT_OK;
+  if (!idx_dev || !out_dev) return set_err(UT_EINVAL, "idx_dev/out_dev is NULL");
+  if (n > UINT64_MAX / t->rb || n > UINT64_MAX / sizeof(int64_t))
+    return set_err(UT_EINVAL, "n*row_bytes overflows");
+  DevState* s;
+  int rc = dev_state(t, &s);
+  if (rc != UT_OK) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t* wide = nullptr;
+  cudaError_t e = cudaMallocFromPoolAsync((void**)&wide, n * sizeof(int64_t), s->pool, st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(UT_ENOMEM, "index scratch of %llu rows", (unsigned long long)n);
+  }
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)s->sms * 8, (n + 255) / 256));
+  ut::k_widen_i32<<<grid, 256, 0, st>>>(idx_dev, wide, n);
+  s->launches += 1;
+  rc = (e = cudaGetLastError()) != cudaSuccess ? cuda_err(e, "k_widen_i32")
+                                               : gather_on(t, s, wide, n, out_dev, st);
+  e = cudaFreeAsync(wide, st);
+  if (rc == UT_OK && e != cudaSuccess) rc = cuda_err(e, "cudaFreeAsync(index scratch)");
+  return rc;
+}
+
 int ut_gather_multi(const ut_table* t, int count, const int* devs, const int64_t* const* idx_dev,
                     const uint64_t* n, void* const* out_dev, const ut_stream_t* streams) {
   if (!t) return set_err(UT_EINVAL, "table is NULL");

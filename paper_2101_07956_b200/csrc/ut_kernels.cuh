@@ -736,6 +736,13 @@ __global__ void __launch_bounds__(512) k_bucket_scatter(GatherArgs a_, int shift
 // so the line two adjacent rows share is requested once instead of twice (two partial requests).
 // Only for 16-B aligned tables and outputs with rb % 16 == 0: a 16-B chunk then lies in one row.
 
+// int32 row ids -> int64 (ut_gather_i32): sign extension, so a negative id stays out of range.
+__global__ void __launch_bounds__(256) k_widen_i32(const int32_t* __restrict__ in, int64_t* __restrict__ out,
+                                                   uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (int64_t)__ldg(in + i);
+}
+
 // Exact order inside each (small) bucket: one thread insertion-sorts its bucket's work items by
 // row id. ends[] = bucket ends after k_bucket_scatter. Buckets above 256 items are left as they
 // are (order only affects how many runs are found, never the result).

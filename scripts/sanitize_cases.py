@@ -1,5 +1,5 @@
 """Tiny cases for compute-sanitizer (memcheck / racecheck / synccheck): every kernel family,
-the reorder stage, run merge, neighbour line sharing, the TMA bulk plan, the paper's kernels, host end-to-end, GPU sampling and
+the reorder stage, run merge, neighbour line sharing, the TMA bulk plan, the paper's kernels, host end-to-end, int32 ids, GPU sampling and
 the cooperative gather (one rank: dispatch, dedup, host fetch, combine)."""
 import os
 import sys
@@ -42,6 +42,8 @@ for rb, off in [(4, 0), (8, 8), (68, 3), (400, 0), (400, 4), (144, 0), (2052, 1)
             t.set_plan(m)
         o = t.gather_host(torch.from_numpy(idx).pin_memory())
         bad += o.numpy().tobytes() != want.tobytes()
+        o = t.gather(torch.from_numpy(idx.astype(np.int32)).cuda())     # ut_gather_i32
+        bad += o.cpu().numpy().tobytes() != want.tobytes()
     hb.close()
 
 g = workloads.CSRGraph(20000, 300000, seed=4)

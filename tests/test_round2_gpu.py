@@ -406,3 +406,27 @@ def test_numa_interleave_managed_table(chunk):
         with pytest.raises(ut.UTError) as ei:
             t.numa_interleave(1)
         assert ei.value.code == ut.UT_ENOTSUP
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("rows,rb", [(40_000, 4), (40_000, 68), (40_000, 400), (40_000, 2052),
+                                     (3_000_000, 512)])   # 1.5 GB: the reorder path
+def test_gather_int32_ids(rows, rb):
+    """ut_gather_i32 (32-bit row ids, SURVEY reading c2): the same bytes and the same
+    out-of-range record as the oracle over the sign-extended list; negative ids stay out of
+    range; n = 0 launches nothing."""
+    hb = workloads.HostBuffer(rows * rb)
+    workloads.fill_table(hb.addr, rows, rb, 400 + rb, threads=0)
+    idx = workloads.uniform_idx(70_001, rows, 401).astype(np.int32)   # >= 64K: reorder on big tables
+    idx[[5, 9, 77]] = [-1, rows, np.iinfo(np.int32).min]
+    want, bad = oracle.gather(hb.addr, rows, rb, idx.astype(np.int64))
+    assert bad == 5
+    with ut.Table(hb.addr, rows, rb) as t:
+        got = t[torch.from_numpy(idx).cuda()].cpu().numpy().reshape(-1)
+        assert got.tobytes() == want.tobytes()
+        assert t.error_pos() == 5
+        if rows * rb > (1 << 30):
+            assert t.stats()["kernel_launches"] >= 5       # widen + the reorder stage + gather
+        empty = t[torch.empty(0, dtype=torch.int32, device="cuda")]
+        assert empty.numel() == 0 and t.error_pos() == -1
+    hb.close()
