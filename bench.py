@@ -361,7 +361,7 @@ def run_reference(args, spec, dist):
             "impl": "reference",
             "config": config_block(spec, timed, args.gpus, args.seed),
             "step_ms": step_stats(step_ms),
-            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1,
+            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "cpu_model": cpu_model(),
                              "kind": "oracle",
                              "sample": f"{args.steps} full minibatches of the workload (GPU 0's "
                                        f"lists of the ut arm), single-threaded plain C"},
@@ -704,7 +704,7 @@ def run_procs(args, spec, dist):
     cpu_base, py_base = None, None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, nl, el = cpu_oracle_rate(hb.addr, spec, lists, args.cpu_budget)
-        cpu_base = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+        cpu_base = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "cpu_model": cpu_model(), "kind": "oracle",
                     "sample": f"{nl} minibatches of the workload in {el:.1f} s, single-threaded plain C"}
         py_base = cpu_staged_baseline(torch, hb.addr, spec, lists, args)
 
@@ -1228,7 +1228,7 @@ def run_box(args, spec, dist=None):
     if N == 1 and not args.no_cpu:
         torch.cuda.set_device(0)
         v, nl, el = cpu_oracle_rate(hb.addr, spec, lists[0], args.cpu_budget)
-        cpu_base = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+        cpu_base = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "cpu_model": cpu_model(), "kind": "oracle",
                     "sample": f"{nl} minibatches of the workload in {el:.1f} s, single-threaded plain C"}
         py_base = cpu_staged_baseline(torch, hb.addr, spec, lists[0], args)
 
@@ -1501,6 +1501,18 @@ class GpuSampling:
                 "oracle_cpu_sample_ms_per_minibatch": round(cpu_ms, 2), "oracle_cores": 1}
 
 
+def cpu_model() -> str:
+    """The host CPU model ("Report T and the CPU model")."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_staged_baseline(torch, table_addr, spec, lists, args):
     """The paper's "Py" path (Fig. 2a): all host cores gather into pinned
     staging, then one H2D DMA. Three forms: sequential (paper-faithful), double-
@@ -1562,7 +1574,7 @@ def cpu_staged_baseline(torch, table_addr, spec, lists, args):
                 nbytes += l.size * rb
         return round(nbytes / sec / 1e9, 3)
 
-    out = {"value": rate(sequential), "unit": "GB/s", "threads": threads,
+    out = {"value": rate(sequential), "unit": "GB/s", "threads": threads, "cpu_model": cpu_model(),
            "kind": "CPU gather into pinned staging + cudaMemcpyAsync H2D (PAPER.md:221-225)",
            "steps": steps, "double_buffered": rate(double_buffered),
            "double_buffered_chunks": chunks}

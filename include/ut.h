@@ -175,7 +175,11 @@ UT_API int ut_gather_multi(const ut_table* t, int count, const int* devs,
  *   out_host  >= n*rb bytes of host memory (caller-owned).
  * If out_host is page-locked and mapped (cudaHostAlloc / cudaHostRegister'ed), idx is copied to
  * the device and the gather kernel stores the rows straight into out_host over the link (one
- * pass, no HBM round trip). Otherwise rows are gathered in
+ * pass, no HBM round trip); every byte of [out_host, out_host + n*rb) must then be mapped (one
+ * allocation, or adjacent ones under UVA — checked allocation by allocation before any work), and
+ * a buffer whose first byte is page-locked but whose range is not returns UT_EINVAL (kernel
+ * stores would fault in the unlocked stretch, and the copy engine refuses a partly locked
+ * destination). Otherwise (pageable memory) rows are gathered in
  * chunks into library-owned device
  * scratch and copied back by the copy engine on a second stream, overlapping the two link
  * directions (UT_HOST_PIPELINE=1 forces this path). Device scratch is owned by the table and

@@ -1275,6 +1275,32 @@ int ut_gather_dn(const ut_table* t, const int64_t* idx_dev, const uint64_t* n_de
   return gather_on(t, s, idx_dev, max_n, out_dev, (cudaStream_t)stream, false, n_dev);
 }
 
+}  // extern "C"
+
+namespace {
+// Is every byte of [a, a+bytes) page-locked and mapped, so that kernel stores through the device
+// address of `a` land in it? Walks the range allocation by allocation (the driver's range
+// attributes): two adjacent pinned allocations qualify only where the host address is the device
+// address (UVA), and an unpinned stretch anywhere in the middle disqualifies the range — the
+// caller then refuses it instead of faulting. Where the driver reports no range extent, the first
+// and last bytes decide.
+bool host_range_mapped(uint64_t a, uint64_t bytes, const void* dev_ptr) {
+  const uint64_t hi = a + bytes;
+  const bool uva = (uint64_t)dev_ptr == a;
+  uint64_t p = a, end = 0;
+  while (p < hi) {
+    if (!pinned_at(p, &end)) return false;
+    if (end == 0) return pinned_at(hi - 1, &end);
+    if (end >= hi) return true;
+    if (!uva) return false;
+    p = end;
+  }
+  return true;
+}
+}  // namespace
+
+extern "C" {
+
 int ut_gather_host(const ut_table* ct, const int64_t* idx_host, uint64_t n, void* out_host,
                    ut_stream_t stream) {
   if (!ct) return set_err(UT_EINVAL, "table is NULL");
@@ -1296,10 +1322,15 @@ int ut_gather_host(const ut_table* ct, const int64_t* idx_host, uint64_t n, void
   void* out_mapped = nullptr;
   if (cudaPointerGetAttributes(&oa, out_host) == cudaSuccess && oa.type == cudaMemoryTypeHost &&
       oa.devicePointer != nullptr) {
-    cudaPointerAttributes ea{};
-    const uint8_t* last = (const uint8_t*)out_host + n * t->rb - 1;
-    if (cudaPointerGetAttributes(&ea, last) == cudaSuccess && ea.type == cudaMemoryTypeHost)
-      out_mapped = oa.devicePointer;
+    if (!host_range_mapped((uint64_t)out_host, n * t->rb, oa.devicePointer)) {
+      cudaGetLastError();
+      // neither path can take it: kernel stores would fault in the unlocked stretch and the copy
+      // engine refuses a destination that is only partly page-locked
+      return set_err(UT_EINVAL, "out_host is only partly page-locked (%llu bytes from its first "
+                     "pinned byte are not one mapped range): pass wholly pinned or wholly "
+                     "pageable memory", (unsigned long long)(n * t->rb));
+    }
+    out_mapped = oa.devicePointer;
   }
   cudaGetLastError();
   // (measured, round 2, papers-shaped managed table: direct stores 36.7 GB/s host->host vs the

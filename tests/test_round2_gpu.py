@@ -2,11 +2,13 @@
 
 * ut_gather_host under every admissible forced plan (the tma4 + host-form deadlock, ADVICE r1);
 * registration of a range that spans other pinned allocations with unpinned gaps (VERDICT r1
-  weak #9): registers the gaps, never faults;
+  weak #9): registers the gaps, never faults; an ut_gather_host output buffer of the same
+  shape takes the copy-engine path instead of storing into the unpinned gap;
 * line sharing with its O(n) selection hash on a sparse selection of a large table;
 * a library-owned (managed) table gathered from several host threads, as bench's box harness
   does, and the harness itself end to end on the tiny config.
 """
+import ctypes
 import json
 import os
 import subprocess
@@ -85,6 +87,51 @@ def test_register_range_spanning_pinned_islands():
         w, _ = oracle.gather(hb.addr + off, n, rb, np.arange(n, dtype=np.int64))
         assert out.cpu().numpy().tobytes() == w.tobytes()
         ut.ut_release(h)
+    hb.close()
+
+
+def test_gather_host_output_spanning_pinned_islands():
+    """ut_gather_host's direct-store path needs every output byte mapped. An output buffer whose
+    first and last pages are pinned (two separate registrations) around an unpinned middle is
+    refused with UT_EINVAL before any work (kernel stores would fault in the gap, the copy engine
+    refuses a partly locked destination) and the CUDA context stays usable; the same buffer made
+    wholly pinned by registering the middle (three adjacent registrations, UVA) is stored
+    directly, and wholly pageable memory takes the copy-engine path."""
+    cudart = torch.cuda.cudart()
+    pg, rb = 4096, 512
+    npages = 64
+    rows = 2000
+    hb = workloads.HostBuffer(rows * rb)
+    workloads.fill_table(hb.addr, rows, rb, 311)
+    idx = workloads.uniform_idx(npages * pg // rb, rows, 312)
+    want, _ = oracle.gather(hb.addr, rows, rb, idx)
+    ob = workloads.HostBuffer(npages * pg, hugepage=False)
+    assert ob.addr % pg == 0
+    flags = 3                                       # cudaHostRegisterPortable | Mapped
+    islands = [(ob.addr, 4 * pg), (ob.addr + (npages - 4) * pg, 4 * pg)]
+    for a, n in islands:
+        assert int(cudart.cudaHostRegister(a, n, flags)) == 0
+    out = torch.frombuffer((ctypes.c_uint8 * (npages * pg)).from_address(ob.addr), dtype=torch.uint8)
+    with ut.Table(hb.addr, rows, rb) as t:
+        for _ in range(2):
+            out.fill_(0xAB)
+            with pytest.raises(ut.UTError) as ei:
+                t.gather_host(torch.from_numpy(idx), out_host=out)
+            assert ei.value.code == -1 and "partly page-locked" in str(ei.value)
+            assert (out.numpy() == 0xAB).all()
+        got = t.gather_host(torch.from_numpy(idx),
+                            out_host=torch.empty((idx.size, rb), dtype=torch.uint8))   # pageable
+        assert got.numpy().tobytes() == want.tobytes()
+        mid = (ob.addr + 4 * pg, (npages - 8) * pg)
+        assert int(cudart.cudaHostRegister(mid[0], mid[1], flags)) == 0
+        out.fill_(0xAB)
+        t.gather_host(torch.from_numpy(idx), out_host=out)
+        assert out.numpy().tobytes() == want.tobytes()
+        cudart.cudaHostUnregister(mid[0])
+    for a, _ in islands:
+        cudart.cudaHostUnregister(a)
+    torch.cuda.synchronize()
+    ob.close()
     hb.close()
 
 
