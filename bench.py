@@ -788,8 +788,23 @@ def run_threads(n: int, fn):
     return res
 
 
+def mem_available() -> int:
+    """Host MemAvailable in bytes (0 when unknown)."""
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
 def box_table(spec: dict, args, ut):
-    """The box's ONE host feature table, shared by every GPU of the process.
+    """The box's host feature table(s), shared by the GPUs of the process. Returns
+    (tables, owners, kind): one table, or with --numa replica one per host NUMA node (SURVEY §8e:
+    "one replica per socket if RAM allows, so every GPU reads locally"; each GPU then gathers from
+    the replica on its own node, `replica_of`).
 
     auto/managed: the paper's own unified-tensor allocation — cudaMallocManaged with
     SetPreferredLocation = CPU and SetAccessedBy = each GPU (Table 2; ut_create
@@ -806,12 +821,39 @@ def box_table(spec: dict, args, ut):
         hb.numa = workloads.interleave(hb.addr, rows * rb)
         workloads.fill_table(hb.addr, rows, rb, args.seed, threads=threads)
         import paper_2101_07956_b200 as _ut
-        return _ut.Table(hb.addr, rows, rb), hb, kind
+        return [_ut.Table(hb.addr, rows, rb)], [hb], kind
+    nodes = workloads.numa_nodes()
+    if kind == "managed" and args.numa == "replica":
+        k = args.numa_replicas or max(nodes, 1)
+        avail = mem_available()
+        if avail and k * rows * rb > 0.85 * avail:
+            note = (f"{k} replicas of {rows * rb / 1e9:.1f} GB do not fit 85 % of MemAvailable "
+                    f"({avail / 1e9:.1f} GB): one table instead")
+            tables, owners, kind = box_table(spec, argparse.Namespace(**{**vars(args), "numa": "auto"}), ut)
+            owners[0].numa = {**owners[0].numa, "replica_request": note}
+            return tables, owners, kind
+        tables, owners = [], []
+        for r in range(k):
+            node = r % max(nodes, 1)
+            table = ut.Table.create(rows, rb, kind)
+            owned = _Owned(table.host_addr)
+            try:
+                table.numa_place(node)
+                how = f"ut_numa_place(node {node})"
+            except ut.UTError as e:
+                how = f"first touch by node {node}'s CPUs (ut_numa_place: {str(e)[:120]})"
+            cpus = workloads.node_cpus(node) or list(range(threads))
+            pinned = workloads.fill_table_on(table.host_addr, rows, rb, args.seed, cpus)
+            owned.numa = {"replica": r, "node": node, "placement": how,
+                          "fill": f"{len(cpus)} threads pinned to node {node}'s CPUs"
+                                  + ("" if pinned else " (pinning failed: unpinned threads)")}
+            tables.append(table)
+            owners.append(owned)
+        return tables, owners, kind
     table = ut.Table.create(rows, rb, kind)
     owned = _Owned(table.host_addr)
     # the box's one table NUMA-interleaved (2-MiB stripes placed by SetPreferredLocation
     # = host NUMA node, before the fill first-touches them); a no-op policy on one-node boxes
-    nodes = workloads.numa_nodes()
     if kind == "managed" and (args.numa == "interleave" or (args.numa == "auto" and nodes > 1)):
         t0 = time.perf_counter()
         try:
@@ -824,7 +866,15 @@ def box_table(spec: dict, args, ut):
     else:
         owned.numa = {"policy": "first touch by the fill threads" + ("" if nodes > 1 else " (one NUMA node)")}
     workloads.fill_table(table.host_addr, rows, rb, args.seed, threads=threads)
-    return table, owned, kind
+    return [table], [owned], kind
+
+
+def replica_of(g_dev: int, g: int, nrep: int) -> int:
+    """The replica GPU g gathers from: the one on its device's NUMA node, else g mod replicas."""
+    if nrep <= 1:
+        return 0
+    node = workloads.gpu_numa_node(g_dev)
+    return node if 0 <= node < nrep and workloads.numa_nodes() >= nrep else g % nrep
 
 
 class BoxWorker:
@@ -1049,11 +1099,14 @@ def run_box(args, spec, dist=None):
     torch.cuda.set_device(0)
     import paper_2101_07956_b200 as ut
     t_reg = time.perf_counter()
-    table, hb, kind = box_table(spec, args, ut)
+    tables, owners, kind = box_table(spec, args, ut)
+    table, hb = tables[0], owners[0]
+    rep = [replica_of(dev_of(g), g, len(tables)) for g in range(N)]
     reg_s = time.perf_counter() - t_reg
     if args.plan:
         for p in args.plan.split(","):
-            table.set_plan(p)
+            for tb in tables:
+                tb.set_plan(p)
     rb = spec["row_bytes"]
     samplers = None
     if args.sample == "gpu":
@@ -1070,7 +1123,7 @@ def run_box(args, spec, dist=None):
         lists = run_threads(N, lambda g: (torch.cuda.set_device(dev_of(g)),
                                           samplers[g].node_lists_for_accounting())[1])
         timed_lists = [lists[0][(args.warmup + s) % count] for s in range(args.steps)]
-    workers = run_threads(N, lambda g: BoxWorker(dev_of(g), torch, table, spec, lists[g], args))
+    workers = run_threads(N, lambda g: BoxWorker(dev_of(g), torch, tables[rep[g]], spec, lists[g], args))
     if samplers is not None:
         for g in range(N):
             workers[g].sampler = samplers[g]
@@ -1085,7 +1138,7 @@ def run_box(args, spec, dist=None):
 
         def mk(g):
             torch.cuda.set_device(dev_of(g))
-            return ut.Coop(table, max_n, rank=g, world=N, sync="device", local=True)
+            return ut.Coop(tables[rep[g]], max_n, rank=g, world=N, sync="device", local=True)
         coops = run_threads(N, mk)
         run_threads(N, lambda g: (torch.cuda.set_device(dev_of(g)), coops[g].open_local(coops)))
         for g in range(N):
@@ -1110,19 +1163,20 @@ def run_box(args, spec, dist=None):
         if coops is not None:     # every rank takes part in every cooperative step
             budget = 0            # -> exactly two lists on every GPU
         parity_lists = sum(run_threads(N, lambda g: (torch.cuda.set_device(dev_of(g)),
-                                                      workers[g].parity(hb.addr, budget))[1]))
+                                                      workers[g].parity(owners[rep[g]].addr, budget))[1]))
 
     clocks = ClockSampler(sorted({dev_of(g) for g in range(N)}))
     clocks.start()
     run_threads(N, lambda g: (torch.cuda.set_device(dev_of(g)), workers[g].warmup()))
-    table.set_plan("timing=on")
+    for tb in tables:
+        tb.set_plan("timing=on")
     devices = sorted({dev_of(g) for g in range(N)})
 
-    def dev_stats():      # the library counts per device
+    def dev_stats():      # the library counts per table and device
         out = []
         for d in devices:
             torch.cuda.set_device(d)
-            out.append(table.stats(reset=True))
+            out.extend(tb.stats(reset=True) for tb in tables)
         return out
     dev_stats()
     coop0 = [c.stats() for c in coops] if coops is not None else None
@@ -1138,7 +1192,8 @@ def run_box(args, spec, dist=None):
     gc.enable()
     clk = clocks.stop()
     stats = dev_stats()
-    table.set_plan("timing=off")
+    for tb in tables:
+        tb.set_plan("timing=off")
     # the link ceiling again, right after timing: box drift shows as a change here
     link_after = run_threads(ndevs, lambda g: link(g, reps=5)) if ndevs > 1 else [link(0, reps=5)]
 
@@ -1267,11 +1322,17 @@ def run_box(args, spec, dist=None):
         "sm_read_ceiling_gbs": round(sm_ceiling, 3),
         "frac_of_sm_read_ceiling": round(value / N / sm_ceiling, 4),
         "plan": plan_label,
-        "table_memory": kind + (" (cudaMallocManaged + SetPreferredLocation=CPU + SetAccessedBy "
-                                "every GPU: one copy for the box)" if kind == "managed" else ""),
-        "numa": {"nodes": workloads.numa_nodes(),
-                 **(hb.numa if isinstance(getattr(hb, "numa", None), dict) else
-                    {"policy": "mbind interleave" if getattr(hb, "numa", 0) > 1 else "first touch"})},
+        "table_memory": kind + ((f" (cudaMallocManaged + SetPreferredLocation=CPU + SetAccessedBy "
+                                 f"every GPU: {len(tables)} replicas, one per NUMA node)") if len(tables) > 1
+                                else " (cudaMallocManaged + SetPreferredLocation=CPU + SetAccessedBy "
+                                     "every GPU: one copy for the box)" if kind == "managed" else ""),
+        "numa": ({"nodes": workloads.numa_nodes(),
+                  "policy": f"one replica per node ({len(tables)} tables, {len(tables)}x the host "
+                            f"memory; SURVEY §8e)", "replicas": [o.numa for o in owners],
+                  "gpu_replica": rep} if len(tables) > 1 else
+                 {"nodes": workloads.numa_nodes(),
+                  **(hb.numa if isinstance(getattr(hb, "numa", None), dict) else
+                     {"policy": "mbind interleave" if getattr(hb, "numa", 0) > 1 else "first touch"})}),
         "roofline": {"bound": "pcie_h2d",
                      "achieved": round(achieved, 3) if achieved is not None else None,
                      "peak": round(link_g, 3), "unit": "GB/s",
@@ -1300,8 +1361,9 @@ def run_box(args, spec, dist=None):
             coops[g].close()
             workers[g].coop = None
     del workers
-    table.close()
-    hb.close()
+    for tb, o in zip(tables, owners):
+        tb.close()
+        o.close()
 
 
 class GpuSampling:
@@ -1631,9 +1693,13 @@ def main(argv=None):
     ap.add_argument("--alloc", default="auto", choices=["auto", "register", "pinned", "managed", "vmm"],
                     help="table memory: auto = managed (the paper's unified tensor) in the threads "
                          "harness; in procs: managed for one rank and a table > 1 GiB, else register")
-    ap.add_argument("--numa", default="auto", choices=["auto", "interleave", "off"],
+    ap.add_argument("--numa", default="auto", choices=["auto", "interleave", "replica", "off"],
                     help="threads harness, managed table: stripe its pages over the host NUMA nodes "
-                         "(auto: when the box has more than one node)")
+                         "(auto: when the box has more than one node), or one replica per node "
+                         "(replica: each GPU reads the copy on its own node, if RAM allows)")
+    ap.add_argument("--numa-replicas", type=int, default=0,
+                    help="--numa replica: number of replicas (0 = one per NUMA node; more than the "
+                         "node count places them round-robin — a harness test on one-node boxes)")
     ap.add_argument("--sample", default="cpu", choices=["cpu", "gpu"],
                     help="cpu: index lists sampled before timing (default, the paper's split); "
                          "gpu: ut_sample inside every timed step (SURVEY NEXT-2; implies --harness procs)")

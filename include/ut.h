@@ -291,6 +291,23 @@ UT_API int ut_mem_advise(const ut_table* t, int advice, int device);
  */
 UT_API int ut_numa_interleave(const ut_table* t, int nodes, uint64_t chunk_bytes);
 
+/*
+ * ut_numa_place — put a whole managed table on ONE host NUMA node ("one replica per
+ * socket if RAM allows, so every GPU reads locally": the caller creates one table per node,
+ * places replica k on node k with this call, fills it, and has each GPU gather from the replica
+ * on its own node). cudaMemAdvise(SetPreferredLocation, {HostNuma, node}) over the table
+ * (PAPER.md:413-416's memAdvise with CUDA's host-NUMA location); SetAccessedBy is unchanged.
+ * Call it between ut_create(src = NULL) and the first write, like ut_numa_interleave.
+ *   t     a UT_ALLOC_MANAGED table.
+ *   node  host NUMA node id >= 0.
+ * The placement is read back at the table's first page. Returns UT_OK, UT_EINVAL (NULL table,
+ * node < 0), UT_ENOTSUP (not a managed table, or the driver accepted the advice without applying
+ * it) or UT_ECUDA (the runtime refused the advice, e.g. a node the host does not have). On either
+ * error the table is advised back to SetPreferredLocation = CPU; the caller may then place it by
+ * first touch from that node's CPUs instead (bench.py --numa replica does).
+ */
+UT_API int ut_numa_place(const ut_table* t, int node);
+
 /* ---- GPU-side neighbour sampling over a host-resident CSR graph -------------
  * The step before the gather that the paper leaves on the CPU. The CSR stays in
  * host memory (pinned in place like a feature table) and GPU threads read it over the link. */

@@ -37,7 +37,7 @@ ABI = ("ut_register", "ut_gather", "ut_gather_host", "ut_release", "ut_error_pos
        "ut_coop_open", "ut_coop_dispatch", "ut_coop_fetch", "ut_coop_combine", "ut_coop_gather",
        "ut_coop_get_stats", "ut_coop_error_pos", "ut_coop_owner", "ut_coop_release",
        "ut_coop_create_partitioned", "ut_coop_partition_ids", "ut_coop_open_local",
-       "ut_gather_multi", "ut_numa_interleave", "ut_gather_i32")
+       "ut_gather_multi", "ut_numa_interleave", "ut_gather_i32", "ut_numa_place")
 
 UT_COOP_HANDLE_BYTES = 64
 
@@ -123,6 +123,8 @@ def _load():
     L.ut_mem_advise.argtypes = [vp, ctypes.c_int, ctypes.c_int]
     L.ut_numa_interleave.restype = ctypes.c_int
     L.ut_numa_interleave.argtypes = [vp, ctypes.c_int, u64]
+    L.ut_numa_place.restype = ctypes.c_int
+    L.ut_numa_place.argtypes = [vp, ctypes.c_int]
     L.ut_graph_release.restype = ctypes.c_int
     L.ut_graph_release.argtypes = [vp]
     L.ut_get_stats.restype = ctypes.c_int
@@ -277,6 +279,11 @@ def ut_mem_advise(t: int, advice: int, device: int) -> int:
 def ut_numa_interleave(t: int, nodes: int, chunk_bytes: int = 0) -> None:
     """Stripe a managed table's pages over host NUMA nodes 0..nodes-1 (before it is filled)."""
     _check(_lib.ut_numa_interleave(t, nodes, chunk_bytes))
+
+
+def ut_numa_place(t: int, node: int) -> None:
+    """Put a whole managed table on one host NUMA node (before it is filled)."""
+    _check(_lib.ut_numa_place(t, node))
 
 
 def ut_gather_multi(t: int, devs: list[int], idx_dev: list[int], n: list[int], out_dev: list[int],
@@ -461,6 +468,10 @@ class Table:
     def numa_interleave(self, nodes: int, chunk_bytes: int = 0) -> None:
         """Managed tables: host pages striped over NUMA nodes 0..nodes-1 (call before filling)."""
         ut_numa_interleave(self.handle, nodes, chunk_bytes)
+
+    def numa_place(self, node: int) -> None:
+        """Managed tables: every host page on NUMA node `node` (call before filling)."""
+        ut_numa_place(self.handle, node)
 
     def stats(self, reset: bool = False) -> dict:
         return ut_get_stats(self.handle, reset)

@@ -1618,13 +1618,14 @@ int ut_mem_advise(const ut_table* t, int advice, int device) {
   return (int)e;
 }
 
-int ut_numa_interleave(const ut_table* t, int nodes, uint64_t chunk_bytes) {
-  if (!t) return set_err(UT_EINVAL, "table is NULL");
-  if (nodes < 1) return set_err(UT_EINVAL, "nodes must be >= 1 (got %d)", nodes);
-  if (t->alloc_kind != UT_ALLOC_MANAGED)
-    return set_err(UT_ENOTSUP, "NUMA striping needs a managed table (ut_create UT_ALLOC_MANAGED)");
-  constexpr uint64_t kBlock = 2ull << 20;
-  const uint64_t chunk = chunk_bytes == 0 ? kBlock : (chunk_bytes + kBlock - 1) / kBlock * kBlock;
+}  // extern "C"
+
+namespace {
+// SetPreferredLocation = host NUMA node node_of(k) for stripe k of `chunk` bytes (k = 0, 1, ...),
+// then read the placement back on the first stripe of each of the first `check` stripes; on any
+// refusal or silent non-application the whole table is advised back to CPU (ut_create's state).
+template <typename NodeOf>
+int numa_advise(const ut_table* t, uint64_t chunk, uint64_t check, NodeOf node_of) {
   auto restore = [&] {
     cudaMemLocation cpu{};
     cpu.type = cudaMemLocationTypeHost;
@@ -1636,7 +1637,7 @@ int ut_numa_interleave(const ut_table* t, int nodes, uint64_t chunk_bytes) {
   for (uint64_t off = 0; off < t->bytes; off += chunk, ++k) {
     cudaMemLocation loc{};
     loc.type = cudaMemLocationTypeHostNuma;
-    loc.id = (int)(k % (uint64_t)nodes);
+    loc.id = node_of(k);
     const cudaError_t e = cudaMemAdvise(t->host + off, std::min(chunk, t->bytes - off),
                                         cudaMemAdviseSetPreferredLocation, loc);
     if (e != cudaSuccess) {
@@ -1647,8 +1648,8 @@ int ut_numa_interleave(const ut_table* t, int nodes, uint64_t chunk_bytes) {
   }
   // Read the advice back: a driver can accept a host-NUMA location and not apply it (measured on
   // this pool's virtualised GPU boxes: cudaSuccess, then no preferred location at all), and a
-  // table whose placement silently stayed elsewhere must not be reported as striped.
-  for (uint64_t j = 0; j < std::min<uint64_t>(k, (uint64_t)nodes); ++j) {
+  // table whose placement silently stayed elsewhere must not be reported as placed.
+  for (uint64_t j = 0; j < std::min<uint64_t>(k, check); ++j) {
     const uint64_t off = j * chunk;
     int typ = -1, id = -1;
     const uint64_t len = std::min<uint64_t>(4096, t->bytes - off);
@@ -1656,16 +1657,38 @@ int ut_numa_interleave(const ut_table* t, int nodes, uint64_t chunk_bytes) {
                                  t->host + off, len) != cudaSuccess ||
         cudaMemRangeGetAttribute(&id, 4, cudaMemRangeAttributePreferredLocationId, t->host + off,
                                  len) != cudaSuccess ||
-        typ != (int)cudaMemLocationTypeHostNuma || id != (int)(j % (uint64_t)nodes)) {
+        typ != (int)cudaMemLocationTypeHostNuma || id != node_of(j)) {
       cudaGetLastError();
       restore();
       return set_err(UT_ENOTSUP, "the driver accepted SetPreferredLocation = host NUMA node %d but "
                      "reports location type %d id %d for stripe %llu: host-NUMA placement is not "
                      "available here (the table keeps SetPreferredLocation = CPU)",
-                     (int)(j % (uint64_t)nodes), typ, id, (unsigned long long)j);
+                     node_of(j), typ, id, (unsigned long long)j);
     }
   }
   return UT_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int ut_numa_interleave(const ut_table* t, int nodes, uint64_t chunk_bytes) {
+  if (!t) return set_err(UT_EINVAL, "table is NULL");
+  if (nodes < 1) return set_err(UT_EINVAL, "nodes must be >= 1 (got %d)", nodes);
+  if (t->alloc_kind != UT_ALLOC_MANAGED)
+    return set_err(UT_ENOTSUP, "NUMA striping needs a managed table (ut_create UT_ALLOC_MANAGED)");
+  constexpr uint64_t kBlock = 2ull << 20;
+  const uint64_t chunk = chunk_bytes == 0 ? kBlock : (chunk_bytes + kBlock - 1) / kBlock * kBlock;
+  return numa_advise(t, chunk, (uint64_t)nodes, [nodes](uint64_t k) { return (int)(k % (uint64_t)nodes); });
+}
+
+int ut_numa_place(const ut_table* t, int node) {
+  if (!t) return set_err(UT_EINVAL, "table is NULL");
+  if (node < 0) return set_err(UT_EINVAL, "node must be >= 0 (got %d)", node);
+  if (t->alloc_kind != UT_ALLOC_MANAGED)
+    return set_err(UT_ENOTSUP, "NUMA placement needs a managed table (ut_create UT_ALLOC_MANAGED)");
+  // one advice over the whole range; its placement read back at the first page
+  return numa_advise(t, t->bytes, 1, [node](uint64_t) { return node; });
 }
 
 int ut_table_get_info(const ut_table* t, ut_table_info* info) {

@@ -455,6 +455,59 @@ def test_numa_interleave_managed_table(chunk):
         assert ei.value.code == ut.UT_ENOTSUP
 
 
+def test_numa_place_managed_table():
+    """ut_numa_place (one replica per socket): a managed table advised onto host NUMA
+    node 0 reads it back as placed, or — where the driver accepts host-NUMA advice without
+    applying it (this pool) — reports UT_ENOTSUP and leaves SetPreferredLocation = CPU; either
+    way the table then gathers exactly. Argument and kind errors are refused."""
+    rows, rb = 1 << 14, 512
+    with ut.Table.create(rows, rb, "managed") as t:
+        try:
+            t.numa_place(0)
+            applied = True
+        except ut.UTError as e:
+            assert e.code == ut.UT_ENOTSUP and "not available" in str(e), e
+            applied = False
+        want = ("cudaMemLocationTypeHostNuma", 0) if applied else ("cudaMemLocationTypeHost", -1)
+        got = _preferred(t.host_addr, 4096)
+        assert got == want or (not applied and got[0] == want[0]), got
+        with pytest.raises(ut.UTError) as ei:       # a node this host does not have
+            t.numa_place(1 << 20)
+        assert ei.value.code in (ut.UT_ECUDA, ut.UT_ENOTSUP)
+        assert _preferred(t.host_addr, 4096)[0] == "cudaMemLocationTypeHost"
+        assert workloads.fill_table_on(t.host_addr, rows, rb, 303, workloads.node_cpus(0) or [0])
+        idx = workloads.uniform_idx(20_000, rows, 304)
+        want, _ = oracle.gather(t.host_addr, rows, rb, idx)
+        assert t[torch.from_numpy(idx).cuda()].cpu().numpy().reshape(-1).tobytes() == want.tobytes()
+        with pytest.raises(ut.UTError) as ei:
+            t.numa_place(-1)
+        assert ei.value.code == ut.UT_EINVAL
+    with ut.Table.create(1024, 64, "pinned") as t:
+        with pytest.raises(ut.UTError) as ei:
+            t.numa_place(0)
+        assert ei.value.code == ut.UT_ENOTSUP
+
+
+@pytest.mark.timeout(600)
+def test_bench_box_harness_numa_replicas():
+    """--numa replica (one replica per socket, each GPU reads its own node's copy):
+    two replicas forced on this one-node pool, two GPU workers on the one GPU, each gathering
+    from its own replica, per-worker parity against that replica's bytes."""
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "products",
+                        "--gpus", "2", "--oversubscribe", "--numa", "replica", "--numa-replicas",
+                        "2", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-e2e"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = json.loads([l for l in p.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["parity_checked"] is True
+    assert line["parity_lists_checked"] >= 4
+    numa = line["numa"]
+    assert len(numa["replicas"]) == 2 and numa["gpu_replica"] == [0, 1], numa
+    assert [r["replica"] for r in numa["replicas"]] == [0, 1]
+    assert "2 replicas" in line["table_memory"]
+    assert line["value"] > 0 and line["gpu_launches"] >= 6
+
+
 @pytest.mark.timeout(300)
 @pytest.mark.parametrize("rows,rb", [(40_000, 4), (40_000, 68), (40_000, 400), (40_000, 2052),
                                      (3_000_000, 512)])   # 1.5 GB: the reorder path

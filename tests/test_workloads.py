@@ -89,3 +89,16 @@ def test_minibatch_structure():
     r0 = set(s.roots(0, rank=0, world=2))
     r1 = set(s.roots(0, rank=1, world=2))
     assert not (r0 & r1)
+
+
+def test_fill_table_on_pinned_threads_matches_fill_table():
+    """The per-node fill (one thread pinned per CPU, first touch on that node) writes exactly the
+    table fill_table writes, for any thread count and a ragged last slice."""
+    rows, rb = 1001, 68
+    a = np.zeros(rows * rb, np.uint8)
+    workloads.fill_table(a, rows, rb, 9)
+    cpus = workloads.node_cpus(0) or [0]
+    for k in (1, 3, len(cpus)):
+        b = np.zeros(rows * rb, np.uint8)
+        assert workloads.fill_table_on(b, rows, rb, 9, (cpus * 3)[:k])
+        assert b.tobytes() == a.tobytes()

@@ -45,6 +45,9 @@ def lib():
         L.gen_fill_table.restype = None
         L.gen_fill_table.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
                                      ctypes.c_uint64, ctypes.c_int]
+        L.gen_fill_table_on.restype = ctypes.c_int
+        L.gen_fill_table_on.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                                        ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int]
         L.gen_fill_rows.restype = None
         L.gen_fill_rows.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
                                     ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int]
@@ -89,6 +92,14 @@ def fill_table(dst, rows: int, rb: int, seed: int, threads: int = 0) -> None:
     if isinstance(dst, np.ndarray):
         assert dst.nbytes >= rows * rb
     lib().gen_fill_table(_addr(dst), rows, rb, seed & 0xFFFFFFFFFFFFFFFF, threads)
+
+
+def fill_table_on(dst, rows: int, rb: int, seed: int, cpus: list[int]) -> bool:
+    """fill_table's content written by one thread pinned to each CPU in ``cpus`` (first touch on
+    their NUMA node). True when every thread ran pinned."""
+    c = np.ascontiguousarray(cpus, dtype=np.int32)
+    return lib().gen_fill_table_on(_addr(dst), rows, rb, seed & 0xFFFFFFFFFFFFFFFF,
+                                   c.ctypes.data, int(c.size)) == 0
 
 
 def fill_rows(dst, ids: np.ndarray, rb: int, seed: int, threads: int = 0) -> None:

@@ -16,7 +16,11 @@
  *   Uniform indices: idx[i] = floor(splitmix64(seed ^ (i * PHI)) * rows / 2^64)
  *   (uniform with replacement over [0, rows), reading R9).
  */
+#define _GNU_SOURCE
+#include <pthread.h>
+#include <sched.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 #include <omp.h>
 
@@ -32,6 +36,21 @@ static inline uint64_t splitmix64(uint64_t x)
 
 uint64_t gen_splitmix64(uint64_t x) { return splitmix64(x); }
 
+static inline void fill_row(uint8_t* row, uint64_t r, uint64_t rb, uint64_t seed)
+{
+    uint64_t base = r * PHI;
+    uint64_t b = 0;
+    for (; b + 8 <= rb; b += 8) {
+        uint64_t w = splitmix64(seed ^ (base + b / 8));
+        memcpy(row + b, &w, 8);
+    }
+    if (b < rb) {
+        uint64_t w = splitmix64(seed ^ (base + b / 8));
+        memcpy(row + b, &w, rb - b);
+    }
+    memcpy(row, &r, rb < 8 ? rb : 8);
+}
+
 /* Fill rows*rb bytes at dst with the self-identifying content. Rows are independent, so the
  * loop is split over `threads` OpenMP threads (threads <= 0: all available). */
 void gen_fill_table(uint8_t* dst, uint64_t rows, uint64_t rb, uint64_t seed, int threads)
@@ -39,21 +58,53 @@ void gen_fill_table(uint8_t* dst, uint64_t rows, uint64_t rb, uint64_t seed, int
     int64_t R = (int64_t)rows;
     int nt = threads > 0 ? threads : omp_get_max_threads();
 #pragma omp parallel for schedule(static, 4096) num_threads(nt)
-    for (int64_t r = 0; r < R; ++r) {
-        uint8_t* row = dst + (uint64_t)r * rb;
-        uint64_t base = (uint64_t)r * PHI;
-        uint64_t b = 0;
-        for (; b + 8 <= rb; b += 8) {
-            uint64_t w = splitmix64(seed ^ (base + b / 8));
-            memcpy(row + b, &w, 8);
-        }
-        if (b < rb) {
-            uint64_t w = splitmix64(seed ^ (base + b / 8));
-            memcpy(row + b, &w, rb - b);
-        }
-        uint64_t id = (uint64_t)r;
-        memcpy(row, &id, rb < 8 ? rb : 8);
+    for (int64_t r = 0; r < R; ++r)
+        fill_row(dst + (uint64_t)r * rb, (uint64_t)r, rb, seed);
+}
+
+/* The same content, written by one thread pinned to each of cpus[0..ncpus) (each a contiguous
+ * slice of rows), so that the pages are first touched -- and, under the default first-touch
+ * policy, placed -- on those CPUs' NUMA node (bench.py --numa replica: one replica per node).
+ * Returns 0, or -1 if a thread could not be started or pinned. */
+struct fill_part { uint8_t* dst; uint64_t lo, hi, rb, seed; int cpu, rc; };
+
+static void* fill_part_run(void* p)
+{
+    struct fill_part* f = (struct fill_part*)p;
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    CPU_SET(f->cpu, &set);
+    f->rc = pthread_setaffinity_np(pthread_self(), sizeof set, &set) == 0 ? 0 : -1;
+    for (uint64_t r = f->lo; r < f->hi; ++r)
+        fill_row(f->dst + r * f->rb, r, f->rb, f->seed);
+    return NULL;
+}
+
+int gen_fill_table_on(uint8_t* dst, uint64_t rows, uint64_t rb, uint64_t seed, const int* cpus, int ncpus)
+{
+    if (ncpus < 1) return -1;
+    struct fill_part* parts = (struct fill_part*)calloc((size_t)ncpus, sizeof *parts);
+    pthread_t* th = (pthread_t*)calloc((size_t)ncpus, sizeof *th);
+    int rc = parts && th ? 0 : -1;
+    int started = 0;
+    const uint64_t per = (rows + (uint64_t)ncpus - 1) / (uint64_t)ncpus;
+    for (int i = 0; rc == 0 && i < ncpus; ++i) {
+        uint64_t lo = (uint64_t)i * per, hi = lo + per;
+        if (lo > rows) lo = rows;
+        if (hi > rows) hi = rows;
+        parts[i] = (struct fill_part){dst, lo, hi, rb, seed, cpus[i], 0};
+        if (pthread_create(&th[i], NULL, fill_part_run, &parts[i]) != 0) rc = -1;
+        else ++started;
     }
+    for (int i = 0; i < started; ++i) {
+        pthread_join(th[i], NULL);
+        if (parts[i].rc != 0) rc = -1;
+    }
+    if (rc != 0 && started < ncpus)      /* finish the rows of threads that never started */
+        gen_fill_table(dst, rows, rb, seed, 0);
+    free(parts);
+    free(th);
+    return rc;
 }
 
 /* Row k of dst = the self-identifying content of table row ids[k] (as gen_fill_table writes it);
