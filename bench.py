@@ -315,15 +315,28 @@ def cpu_oracle_rate(table_addr: int, spec: dict, lists: list[np.ndarray], budget
     import oracle
     rb = spec["row_bytes"]
     out = np.empty(max(l.size for l in lists) * rb, dtype=np.uint8)
-    done_bytes, done_lists, t0 = 0, 0, time.perf_counter()
-    while True:
-        l = lists[done_lists % len(lists)]
-        oracle.gather_into(table_addr, spec["rows"], rb, l, out)
-        done_bytes += l.size * rb
-        done_lists += 1
-        el = time.perf_counter() - t0
-        if el >= budget_s or done_lists >= 64 * len(lists):
-            break
+    # one core on the table's NUMA node (node 0: where the fill first-touched it, or
+    # one of the nodes it is striped over); this thread only, restored afterwards
+    old_aff = os.sched_getaffinity(0)
+    cpu = (workloads.node_cpus(0) or sorted(old_aff))[0]
+    try:
+        os.sched_setaffinity(0, {cpu})
+    except OSError:
+        cpu = None
+    try:
+        done_bytes, done_lists, t0 = 0, 0, time.perf_counter()
+        while True:
+            l = lists[done_lists % len(lists)]
+            oracle.gather_into(table_addr, spec["rows"], rb, l, out)
+            done_bytes += l.size * rb
+            done_lists += 1
+            el = time.perf_counter() - t0
+            if el >= budget_s or done_lists >= 64 * len(lists):
+                break
+    finally:
+        if cpu is not None:
+            os.sched_setaffinity(0, old_aff)
+    cpu_oracle_rate.pinned_cpu = cpu
     return done_bytes / el / 1e9, done_lists, el
 
 
@@ -1284,7 +1297,8 @@ def run_box(args, spec, dist=None):
         torch.cuda.set_device(0)
         v, nl, el = cpu_oracle_rate(hb.addr, spec, lists[0], args.cpu_budget)
         cpu_base = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "cpu_model": cpu_model(), "kind": "oracle",
-                    "sample": f"{nl} minibatches of the workload in {el:.1f} s, single-threaded plain C"}
+                    "sample": f"{nl} minibatches of the workload in {el:.1f} s, single-threaded plain C",
+                    "pinned_cpu": getattr(cpu_oracle_rate, "pinned_cpu", None)}
         py_base = cpu_staged_baseline(torch, hb.addr, spec, lists[0], args)
 
     cfg = config_block(spec, timed_lists, N, seed)
