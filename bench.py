@@ -254,6 +254,38 @@ def h2d_ceiling(torch, nbytes: int = 1 << 30, reps: int = 10, stream=None, host=
     return best
 
 
+def h2d_ceiling_by_node(torch, dev: int, nbytes: int = 1 << 30):
+    """R_link measured once from the table's NUMA placement (node 0, where the fill
+    puts or starts it) and once from the GPU-local node — a pinned 1-GiB source bound to each
+    node (mbind before first touch, then cudaHostRegister). None on a one-node box (the same
+    figure as h2d_memcpy_gbs)."""
+    if workloads.numa_nodes() <= 1:
+        return None
+    cudart = torch.cuda.cudart()
+    gnode = workloads.gpu_numa_node(dev)
+    out = {"gpu_node": gnode, "gbs": {}}
+    for label, node in (("table_node_0", 0), ("gpu_local", gnode)):
+        if node < 0 or (label == "gpu_local" and node == 0):
+            continue
+        hb = workloads.HostBuffer(nbytes)
+        try:
+            if not workloads.bind_node(hb.addr, nbytes, node):
+                out["gbs"][label] = None
+                continue
+            hb.array()[:] = 1
+            if int(cudart.cudaHostRegister(hb.addr, nbytes, 0)) != 0:
+                out["gbs"][label] = None
+                continue
+            try:
+                view = torch.frombuffer((ctypes.c_uint8 * nbytes).from_address(hb.addr), dtype=torch.uint8)
+                out["gbs"][label] = round(h2d_ceiling(torch, nbytes, 5, host=view), 3)
+            finally:
+                cudart.cudaHostUnregister(hb.addr)
+        finally:
+            hb.close()
+    return out
+
+
 def sm_read_ceiling(torch, ut, nbytes: int = 1 << 30, reps: int = 5) -> float:
     """The SM-issued sysmem read ceiling (GB/s): this library's own kernel gathering 512-B rows
     in order from a 1-GiB pinned buffer (whole 128-B lines, sequential addresses) — the most a
@@ -1166,6 +1198,10 @@ def run_box(args, spec, dist=None):
         torch.cuda.set_device(dev_of(g))
         return h2d_ceiling(torch, stream=workers[g].stream, reps=reps)
     link_solo = [link(g) for g in range(ndevs)]
+    link_nodes = []
+    for g in range(ndevs):
+        torch.cuda.set_device(dev_of(g))
+        link_nodes.append(h2d_ceiling_by_node(torch, dev_of(g)))
     link_conc = run_threads(ndevs, link) if ndevs > 1 else list(link_solo)
     torch.cuda.set_device(0)
     sm_ceiling = sm_read_ceiling(torch, ut)
@@ -1328,6 +1364,8 @@ def run_box(args, spec, dist=None):
         "h2d_memcpy_gbs": round(link_g, 3),
         "h2d_memcpy_gbs_per_gpu": [round(x, 3) for x in link_solo],
         "h2d_memcpy_concurrent_gbs": round(box_link, 3),
+        "h2d_memcpy_gbs_by_numa_node": (link_nodes if any(x is not None for x in link_nodes) else
+                                        "one NUMA node: the same as h2d_memcpy_gbs"),
         "h2d_memcpy_gbs_after_timing": [round(x, 3) for x in link_after],
         "host_dram_read_gbs": dram,
         "box_roofline_gbs": round(min(box_link, dram), 3) if dram else round(box_link, 3),

@@ -62,6 +62,8 @@ def lib():
                                           ctypes.c_double, ctypes.c_uint64, ctypes.c_int]
         L.gen_numa_nodes.restype = ctypes.c_int
         L.gen_numa_nodes.argtypes = []
+        L.gen_bind_node.restype = ctypes.c_int
+        L.gen_bind_node.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int]
         L.gen_interleave.restype = ctypes.c_int
         L.gen_interleave.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
         L.gen_map.restype = ctypes.c_void_p
@@ -128,6 +130,11 @@ def interleave(addr: int, nbytes: int) -> int:
     """Interleave the pages of [addr, addr+nbytes) over all NUMA nodes before first touch.
     Returns the node count used (0: single node, nothing to do; -1: mbind failed)."""
     return int(lib().gen_interleave(addr, nbytes))
+
+
+def bind_node(addr: int, nbytes: int, node: int) -> bool:
+    """Bind the pages of [addr, addr+nbytes) to one NUMA node before first touch."""
+    return int(lib().gen_bind_node(addr, nbytes, node)) == 0
 
 
 def gpu_numa_node(device_index: int = 0) -> int:

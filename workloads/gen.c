@@ -253,6 +253,15 @@ int gen_numa_nodes(void)
     return n;
 }
 
+/* mbind(MPOL_BIND) of [addr, addr+bytes) to one node before first touch. 0 on success. */
+int gen_bind_node(void* addr, uint64_t bytes, int node)
+{
+    if (node < 0 || node >= 1024) return -1;
+    unsigned long mask[16] = {0};
+    mask[node / 64] |= 1ul << (node % 64);
+    return syscall(SYS_mbind, addr, bytes, 2 /* MPOL_BIND */, mask, 1024ul, 0u) == 0 ? 0 : -1;
+}
+
 int gen_interleave(void* addr, uint64_t bytes)
 {
     int nodes = gen_numa_nodes();
