@@ -505,7 +505,13 @@ UT_API int ut_coop_combine(ut_coop* c, void* out_dev, ut_stream_t stream);
 /* The three phases with device-side barriers between them (every rank calls it for the step).
  * Returns UT_OK, UT_EINVAL, UT_ENOTSUP (no stream memory operations) or UT_ECUDA. On UT_EINVAL
  * for n > max_n or a NULL buffer, the rank still took part in the step with n = 0 (its peers'
- * device waits are satisfied); out_dev is untouched. */
+ * device waits are satisfied); out_dev is untouched. A failure inside the fetch phase still
+ * writes this rank's barrier-1 flags. Any other failure before barrier 0 — the wrong current
+ * device, unopened peers, a launch error of the dispatch (a broken context) — returns without
+ * joining the step: its peers' streams then wait at barrier 0 until the process (or the whole
+ * job) is torn down. This is deliberate — joining the step without having dispatched would let
+ * the peers combine stale rows from this rank's staging silently — so a rank that sees such an
+ * error must abort the job rather than continue. */
 UT_API int ut_coop_gather(ut_coop* c, const int64_t* idx_dev, uint64_t n, void* out_dev,
                           ut_stream_t stream);
 
