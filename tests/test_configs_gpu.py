@@ -50,3 +50,25 @@ def test_sweep_table_16gib(rb):
     lists = bench.make_index_lists(spec, 0, 1, 1, 7, 1)
     lists[0][:3] = [0, spec["rows"] - 1, spec["rows"] // 2]       # first and last row of 2^32 for 4 B
     _check_lists(spec, lists, extra_plans=("reorder=off",))
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("config", ["reddit", "products", "papers"])
+def test_paper_shaped_configs_managed_table(config):
+    """The bench default's table memory at full size: the paper's managed unified tensor
+    (ut_create MANAGED, SetPreferredLocation = CPU, filled in place), the auto plan bench.py
+    times (line sharing on products), whole minibatches of GPU 0 and of rank 1 of 2, byte for
+    byte against the oracle over the same host bytes."""
+    spec = bench.workload_spec(config)
+    rows, rb = spec["rows"], spec["row_bytes"]
+    lists = bench.make_index_lists(spec, 0, 1, 2, 2101, 1)
+    lists += bench.make_index_lists(spec, 1, 2, 1, 2101, 1)
+    with ut.Table.create(rows, rb, "managed") as t:
+        workloads.fill_table(t.host_addr, rows, rb, 2101, threads=0)
+        for l in lists:
+            out = t.gather(torch.from_numpy(l).cuda())
+            want, bad = oracle.gather(t.host_addr, rows, rb, l)
+            assert out.cpu().numpy().reshape(-1).tobytes() == want.tobytes(), f"{config} plan={t.plan}"
+            assert t.error_pos() == bad == -1
+        if config == "products":
+            assert t.stats()["share_gathers"] >= len(lists)
