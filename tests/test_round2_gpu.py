@@ -530,3 +530,39 @@ def test_gather_int32_ids(rows, rb):
         empty = t[torch.empty(0, dtype=torch.int32, device="cuda")]
         assert empty.numel() == 0 and t.error_pos() == -1
     hb.close()
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("rb,plan", [(4, "auto"), (4, "reorder=off"), (16, "reorder=off")])
+def test_gather_beyond_2pow31_rows(rb, plan):
+    """Maximum sizes: one gather of n = 2^31 + 4099 rows (16 GiB of int64 ids in HBM) — past every
+    32-bit row count. "auto" on this 256-MiB table of 4-B rows takes the reorder stage, which
+    splits the gather into 2^31-row chunks; "reorder=off" runs the plain kernel over the whole n
+    (64-bit tile indexing). Every output row is checked through the self-identifying content
+    (its first bytes = the low bytes of the row id fetched), and sampled positions — both sides
+    of the 2^31 boundary, the ends, 2^20 random ones — byte for byte against the oracle."""
+    rows = 1 << 26
+    n = (1 << 31) + 4099
+    hb = workloads.HostBuffer(rows * rb)
+    workloads.fill_table(hb.addr, rows, rb, 601, threads=0)
+    idx = workloads.uniform_idx(n, rows, 602)
+    idx[-3:] = [rows - 1, 0, rows - 1]
+    with ut.Table(hb.addr, rows, rb) as t:
+        t.set_plan(plan)
+        idx_d = torch.from_numpy(idx).cuda()
+        out = t.gather(idx_d)
+        assert t.error_pos() == -1
+        del idx_d
+        got = out.cpu().numpy().reshape(n, rb)
+        del out
+    torch.cuda.empty_cache()
+    ids = got[:, :4].copy().view(np.uint32).reshape(-1)
+    assert np.array_equal(ids, idx.astype(np.uint32)), "a row id decodes wrong"
+    del ids
+    rng = np.random.default_rng(603)
+    pos = np.concatenate([np.arange(1000), np.arange((1 << 31) - 1000, (1 << 31) + 1000),
+                          np.arange(n - 1000, n), rng.integers(0, n, 1 << 20)])
+    want, bad = oracle.gather(hb.addr, rows, rb, idx[pos])
+    assert bad == -1
+    assert got[pos].reshape(-1).tobytes() == want.tobytes()
+    hb.close()
