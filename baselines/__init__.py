@@ -23,15 +23,21 @@ def build(force: bool = False) -> str:
     return _SO
 
 
-def cpu_staged_gather(table_addr: int, rb: int, idx_addr: int, n: int, staging_addr: int,
-                      threads: int = 0) -> None:
+def lib():
+    """The compiled baselines (loaded once; call it before concurrent use)."""
     global _lib
     if _lib is None:
-        _lib = ctypes.CDLL(build())
-        _lib.cpu_staged_gather.restype = None
-        _lib.cpu_staged_gather.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
-                                           ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int]
-    _lib.cpu_staged_gather(table_addr, rb, idx_addr, n, staging_addr, threads)
+        L = ctypes.CDLL(build())
+        L.cpu_staged_gather.restype = None
+        L.cpu_staged_gather.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
+                                        ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int]
+        _lib = L
+    return _lib
+
+
+def cpu_staged_gather(table_addr: int, rb: int, idx_addr: int, n: int, staging_addr: int,
+                      threads: int = 0) -> None:
+    lib().cpu_staged_gather(table_addr, rb, idx_addr, n, staging_addr, threads)
 
 
 def host_read_gbs(addr: int, nbytes: int, threads: int = 0, reps: int = 3) -> float:

@@ -752,6 +752,7 @@ def run_procs(args, spec, dist):
         cpu_base = {"value": round(v, 4), "unit": "GB/s", "cores": 1, "cpu_model": cpu_model(), "kind": "oracle",
                     "sample": f"{nl} minibatches of the workload in {el:.1f} s, single-threaded plain C"}
         py_base = cpu_staged_baseline(torch, hb.addr, spec, lists, args)
+        py_base.pop("_raw", None)
 
     if rank == 0:
         n_launch = int(launches)
@@ -1336,6 +1337,10 @@ def run_box(args, spec, dist=None):
                     "sample": f"{nl} minibatches of the workload in {el:.1f} s, single-threaded plain C",
                     "pinned_cpu": getattr(cpu_oracle_rate, "pinned_cpu", None)}
         py_base = cpu_staged_baseline(torch, hb.addr, spec, lists[0], args)
+        py_base.pop("_raw", None)
+    elif N > 1 and not args.no_cpu and coops is None and samplers is None:
+        py_base = cpu_staged_box(torch, run_threads, N, lambda g: owners[rep[g]].addr, spec, lists,
+                                 args, lambda g: torch.cuda.set_device(dev_of(g)))
 
     cfg = config_block(spec, timed_lists, N, seed)
     if samplers is not None and args.pipeline:
@@ -1616,29 +1621,48 @@ class GpuSampling:
 
 
 def cpu_model() -> str:
-    """The host CPU model ("Report T and the CPU model")."""
+    """The host CPU model ("Report T and the CPU model"): the model name, and — since
+    virtualised hosts report a generic name — family/model numbers and the L3 size, which decide
+    how much of a CPU gather's staging stays in cache."""
+    name, fam, mod = "unknown", "?", "?"
     try:
         with open("/proc/cpuinfo") as f:
             for line in f:
-                if line.startswith("model name"):
-                    return line.split(":", 1)[1].strip()
+                k, _, v = line.partition(":")
+                k = k.strip()
+                if k == "model name" and name == "unknown":
+                    name = v.strip()
+                elif k == "cpu family" and fam == "?":
+                    fam = v.strip()
+                elif k == "model" and mod == "?":
+                    mod = v.strip()
+                if name != "unknown" and fam != "?" and mod != "?":
+                    break
     except OSError:
         pass
-    return "unknown"
+    try:
+        with open("/sys/devices/system/cpu/cpu0/cache/index3/size") as f:
+            l3 = f.read().strip()
+    except OSError:
+        l3 = "?"
+    return f"{name} (family {fam} model {mod}, L3 {l3})"
 
 
-def cpu_staged_baseline(torch, table_addr, spec, lists, args):
+def cpu_staged_baseline(torch, table_addr, spec, lists, args, threads=None, barrier=None):
     """The paper's "Py" path (Fig. 2a): all host cores gather into pinned
     staging, then one H2D DMA. Three forms: sequential (paper-faithful), double-
     buffered (chunk k+1 gathered while chunk k is in flight: the stronger CPU-centric baseline),
     and pageable (Listing 1 literally, `features[neighbor_id].to("cuda")`, PAPER.md:315-316,
-    torch's own CPU index_select into pageable memory)."""
+    torch's own CPU index_select into pageable memory). At k GPUs ("T = cores/k per
+    rank") one call per GPU runs concurrently with `threads` host threads each, `barrier`
+    starting every form on all GPUs together; the raw (bytes, seconds) of each form are returned
+    under "_raw" for the box aggregate, and the pageable form is skipped."""
     import baselines
     rb = spec["row_bytes"]
     max_n = max(l.size for l in lists)
     staging = torch.empty(max_n * rb, dtype=torch.uint8, pin_memory=True)
     dev = torch.empty(max_n * rb, dtype=torch.uint8, device="cuda")
-    threads = os.cpu_count() or 1
+    threads = threads or os.cpu_count() or 1
     steps = min(len(lists), max(3, args.steps // 2))
     chunks = 8
     copy_stream = torch.cuda.Stream()
@@ -1675,8 +1699,13 @@ def cpu_staged_baseline(torch, table_addr, spec, lists, args):
     def pageable(l):
         table_view[torch.from_numpy(l)].to("cuda")
 
-    def rate(fn):
+    raw = {}
+
+    def rate(fn, name):
         sec, nbytes = 0.0, 0
+        if barrier is not None:
+            torch.cuda.synchronize()
+            barrier.wait()
         for s in range(steps + 1):
             l = lists[s % len(lists)]
             torch.cuda.synchronize()
@@ -1686,15 +1715,43 @@ def cpu_staged_baseline(torch, table_addr, spec, lists, args):
             if s > 0:
                 sec += time.perf_counter() - t0
                 nbytes += l.size * rb
+        raw[name] = (nbytes, sec)
         return round(nbytes / sec / 1e9, 3)
 
-    out = {"value": rate(sequential), "unit": "GB/s", "threads": threads, "cpu_model": cpu_model(),
+    out = {"value": rate(sequential, "sequential"), "unit": "GB/s", "threads": threads,
+           "cpu_model": cpu_model(),
            "kind": "CPU gather into pinned staging + cudaMemcpyAsync H2D (PAPER.md:221-225)",
-           "steps": steps, "double_buffered": rate(double_buffered),
+           "steps": steps, "double_buffered": rate(double_buffered, "double_buffered"),
            "double_buffered_chunks": chunks}
-    out["pageable"] = rate(pageable)
-    out["pageable_kind"] = "torch CPU index_select + pageable .to('cuda') (Listing 1, PAPER.md:315-316)"
+    if barrier is None:
+        out["pageable"] = rate(pageable, "pageable")
+        out["pageable_kind"] = "torch CPU index_select + pageable .to('cuda') (Listing 1, PAPER.md:315-316)"
+    out["_raw"] = raw
     return out
+
+
+def cpu_staged_box(torch, run_threads_fn, n, addr_of, spec, lists, args, set_dev):
+    """SURVEY §8d's CPU-centric baseline at k = n GPUs: every GPU's Py path at once, cores/k host
+    threads each; value = Σ bytes ÷ max seconds per form, with the per-GPU rates beside it."""
+    import baselines
+    baselines.lib()
+    per = max(1, (os.cpu_count() or 1) // n)
+    bar = threading.Barrier(n)
+    res = run_threads_fn(n, lambda g: (set_dev(g), cpu_staged_baseline(
+        torch, addr_of(g), spec, lists[g], args, threads=per, barrier=bar))[1])
+
+    def agg(name):
+        b = sum(r["_raw"][name][0] for r in res)
+        sec = max(r["_raw"][name][1] for r in res)
+        return round(b / sec / 1e9, 3)
+    return {"value": agg("sequential"), "unit": "GB/s", "gpus": n, "threads_per_gpu": per,
+            "cpu_model": cpu_model(),
+            "kind": "CPU gather into pinned staging + cudaMemcpyAsync H2D (PAPER.md:221-225), "
+                    "every GPU at once, cores/k threads per GPU (SURVEY §8d)",
+            "double_buffered": agg("double_buffered"),
+            "per_gpu_sequential": [r["value"] for r in res],
+            "per_gpu_double_buffered": [r["double_buffered"] for r in res],
+            "steps": res[0]["steps"], "double_buffered_chunks": res[0]["double_buffered_chunks"]}
 
 
 def self_launch(args, argv) -> int:

@@ -246,6 +246,24 @@ def test_bench_box_harness_two_workers_one_gpu():
     assert line["step_ms"]["n"] == 6 and line["roofline"]["frac"] > 0
 
 
+@pytest.mark.timeout(600)
+def test_bench_box_harness_cpu_baseline_at_two_gpus():
+    """SURVEY §8d's CPU-centric baseline at k GPUs: every worker's CPU gather + H2D DMA at once
+    with cores/k host threads each, aggregated as Σ bytes / max seconds (two workers on this
+    one GPU: a harness test of the k > 1 form, not a scaling measurement)."""
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--oversubscribe", "--config", "products", "--steps", "6", "--warmup", "3",
+                        "--no-e2e", "--max-lists", "9"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = json.loads([l for l in p.stdout.splitlines() if l.startswith("{")][-1])
+    py = line["py_baseline"]
+    assert py["gpus"] == 2 and py["threads_per_gpu"] == max(1, (os.cpu_count() or 1) // 2)
+    assert len(py["per_gpu_sequential"]) == 2 and len(py["per_gpu_double_buffered"]) == 2
+    assert py["value"] > 0 and py["double_buffered"] > 0 and "_raw" not in py
+    assert line["cpu_baseline"] is None          # the oracle's 1-core figure is an N = 1 item
+
+
 @pytest.mark.timeout(300)
 @pytest.mark.parametrize("world", [2, 3])
 def test_coop_in_process_ranks(world):
