@@ -286,6 +286,46 @@ def h2d_ceiling_by_node(torch, dev: int, nbytes: int = 1 << 30):
     return out
 
 
+def box_topology(torch, devs: list[int]) -> dict:
+    """the host-link facts behind R_link / R_concurrent — each GPU's PCI address,
+    NUMA node and PCIe link generation / width (read right after the memcpy ceiling, while the
+    link is up to speed), and for N > 1 the nearest common ancestor of every GPU pair (same PCIe
+    switch, host bridge, NUMA node or across sockets: which GPUs share an uplink)."""
+    try:
+        import pynvml as nv
+        nv.nvmlInit()
+    except Exception as e:  # noqa: BLE001 - context only, never fatal
+        return {"error": f"nvml: {type(e).__name__}: {e}"[:200]}
+    names = {nv.NVML_TOPOLOGY_INTERNAL: "same board", nv.NVML_TOPOLOGY_SINGLE: "one PCIe switch",
+             nv.NVML_TOPOLOGY_MULTIPLE: "several PCIe switches",
+             nv.NVML_TOPOLOGY_HOSTBRIDGE: "same host bridge", nv.NVML_TOPOLOGY_NODE: "same NUMA node",
+             nv.NVML_TOPOLOGY_SYSTEM: "across sockets"}
+    out, handles = {"gpus": []}, {}
+    try:
+        for d in devs:
+            p = torch.cuda.get_device_properties(d)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+            handles[d] = h
+            out["gpus"].append({
+                "device": d, "pci": bus[4:], "numa_node": workloads.gpu_numa_node(d),
+                "pcie_gen": nv.nvmlDeviceGetCurrPcieLinkGeneration(h),
+                "pcie_gen_max": nv.nvmlDeviceGetMaxPcieLinkGeneration(h),
+                "pcie_width": nv.nvmlDeviceGetCurrPcieLinkWidth(h),
+                "pcie_width_max": nv.nvmlDeviceGetMaxPcieLinkWidth(h)})
+        if len(devs) > 1:
+            out["pairs"] = {f"{a}-{b}": names.get(nv.nvmlDeviceGetTopologyCommonAncestor(handles[a], handles[b]), "?")
+                            for i, a in enumerate(devs) for b in devs[i + 1:]}
+    except Exception as e:  # noqa: BLE001
+        out["error"] = f"{type(e).__name__}: {e}"[:200]
+    finally:
+        try:
+            nv.nvmlShutdown()
+        except Exception:  # noqa: BLE001
+            pass
+    return out
+
+
 def sm_read_ceiling(torch, ut, nbytes: int = 1 << 30, reps: int = 5) -> float:
     """The SM-issued sysmem read ceiling (GB/s): this library's own kernel gathering 512-B rows
     in order from a 1-GiB pinned buffer (whole 128-B lines, sequential addresses) — the most a
@@ -1204,6 +1244,7 @@ def run_box(args, spec, dist=None):
         torch.cuda.set_device(dev_of(g))
         link_nodes.append(h2d_ceiling_by_node(torch, dev_of(g)))
     link_conc = run_threads(ndevs, link) if ndevs > 1 else list(link_solo)
+    topo = box_topology(torch, sorted({dev_of(g) for g in range(N)}))
     torch.cuda.set_device(0)
     sm_ceiling = sm_read_ceiling(torch, ut)
 
@@ -1369,6 +1410,7 @@ def run_box(args, spec, dist=None):
         "h2d_memcpy_gbs": round(link_g, 3),
         "h2d_memcpy_gbs_per_gpu": [round(x, 3) for x in link_solo],
         "h2d_memcpy_concurrent_gbs": round(box_link, 3),
+        "host_links": topo,
         "h2d_memcpy_gbs_by_numa_node": (link_nodes if any(x is not None for x in link_nodes) else
                                         "one NUMA node: the same as h2d_memcpy_gbs"),
         "h2d_memcpy_gbs_after_timing": [round(x, 3) for x in link_after],

@@ -228,6 +228,8 @@ def test_bench_box_harness_tiny():
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
     assert set(line["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
     assert line["clocks"]["samples"] >= 1
+    g0 = line["host_links"]["gpus"][0]           # the link facts behind R_link
+    assert g0["pcie_gen"] >= 1 and g0["pcie_width"] >= 1 and g0["pci"].count(":") == 2
 
 
 @pytest.mark.timeout(600)
