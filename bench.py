@@ -313,6 +313,10 @@ def box_topology(torch, devs: list[int]) -> dict:
                 "pcie_gen_max": nv.nvmlDeviceGetMaxPcieLinkGeneration(h),
                 "pcie_width": nv.nvmlDeviceGetCurrPcieLinkWidth(h),
                 "pcie_width_max": nv.nvmlDeviceGetMaxPcieLinkWidth(h)})
+            g = out["gpus"][-1]       # context, not the roofline
+            gts = {1: 2.5, 2: 5.0, 3: 8.0, 4: 16.0, 5: 32.0, 6: 64.0}.get(g["pcie_gen"])
+            enc = 0.8 if g["pcie_gen"] in (1, 2) else (242 / 256 if g["pcie_gen"] == 6 else 128 / 130)
+            g["theoretical_gbs_per_direction"] = round(gts * g["pcie_width"] * enc / 8, 2) if gts else None
         if len(devs) > 1:
             out["pairs"] = {f"{a}-{b}": names.get(nv.nvmlDeviceGetTopologyCommonAncestor(handles[a], handles[b]), "?")
                             for i, a in enumerate(devs) for b in devs[i + 1:]}
@@ -380,6 +384,17 @@ def ncu_traffic(workload: str, plan: str, table_memory: str, args) -> dict:
             (rec["pcie_read_bytes_per_launch"] - rec["sysmem_bytes_per_launch"]) / req, 2)
         detail["payload_bytes_per_request"] = round(alg / req, 1)
     return {"traffic": rec["hbm_bytes_per_launch"], "traffic_detail": detail}
+
+
+def transferred_ncu(value: float, rec: dict) -> dict:
+    """transferred GB/s = sysmem sector bytes / time, cross-checked with the PCIe
+    read bytes — this run's useful GB/s scaled by the committed ncu capture's per-launch ratios
+    for the same workload, plan and table memory (absent when no capture matches)."""
+    d = (rec or {}).get("traffic_detail") or {}
+    if not d.get("sectors_over_algorithmic"):
+        return {}
+    return {"transferred_gbs_ncu_sectors": round(value * d["sectors_over_algorithmic"], 3),
+            "pcie_read_gbs_ncu": round(value * d["pcie_read_over_algorithmic"], 3)}
 
 
 def cpu_oracle_rate(table_addr: int, spec: dict, lists: list[np.ndarray], budget_s: float):
@@ -1390,6 +1405,7 @@ def run_box(args, spec, dist=None):
                   if cfg.get("mb_per_step_per_gpu") else None)
     link_g = statistics.mean(link_solo)
     box_link = sum(link_conc)
+    ncu_rec = ncu_traffic(spec["workload"], plan_label, kind, args)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": N,
         "steps": args.steps, "warmup": args.warmup,
@@ -1405,6 +1421,7 @@ def run_box(args, spec, dist=None):
                      "region_ms": [round(m, 4) for m in all_ms]}),
         "per_gpu_gbs": [round(x, 3) for x in per_gpu],
         "transferred_gbs_sector_floor": round(value * sect_ratio, 3) if sect_ratio else None,
+        **transferred_ncu(value, ncu_rec),
         "line_requests_per_s": (round(cfg["line_requests_per_step"] * N / (max(dev_ms) / args.steps / 1e3))
                                 if cfg.get("line_requests_per_step") else None),
         "h2d_memcpy_gbs": round(link_g, 3),
@@ -1436,7 +1453,7 @@ def run_box(args, spec, dist=None):
                      "achieved": round(achieved, 3) if achieved is not None else None,
                      "peak": round(link_g, 3), "unit": "GB/s",
                      "frac": round(achieved / link_g, 4) if achieved is not None else None,
-                     **ncu_traffic(spec["workload"], plan_label, kind, args),
+                     **ncu_rec,
                      "kernel": f"gather {plan_label} (device time of the gather kernels, share "
                                f"hash/mark included, CUDA events on the launch stream; per GPU)",
                      "timed_launches": kern_n,
