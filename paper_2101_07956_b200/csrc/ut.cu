@@ -695,12 +695,14 @@ int tensor_map(const ut_table* t, DevState* s) {
 }
 
 int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n, void* out_dev,
-              cudaStream_t st, bool host_out = false, const uint64_t* n_dev = nullptr) {
+              cudaStream_t st, bool host_out = false, const uint64_t* n_dev = nullptr,
+              uint64_t pos0 = 0) {
   Plan p;
   if (!choose_plan((uint64_t)t->host, t->rows, t->rb, (uint64_t)out_dev, t->forced, &p) &&
       !choose_plan((uint64_t)t->host, t->rows, t->rb, (uint64_t)out_dev, P_AUTO, &p))
     return set_err(UT_EINVAL, "no admissible plan");
   ut::GatherArgs a{s->dev_base, t->rows, t->rb, idx_dev, n, (uint64_t)out_dev, s->err, nullptr, n_dev};
+  a.pos0 = pos0;          // this list's offset in the caller's (ut_gather_host's chunks)
   if (p.kind == P_TMA4) {
     int rc = tensor_map(t, s);
     if (rc != UT_OK) return rc;
@@ -751,6 +753,7 @@ int gather_on(const ut_table* t, DevState* s, const int64_t* idx_dev, uint64_t n
     ut::GatherArgs c = a;
     c.idx = idx_dev + off;
     c.n = cnt_n;
+    c.pos0 = a.pos0 + off;      // error positions stay positions of the whole list
     c.out = (uint64_t)out_dev + off * t->rb;
     c.perm = perm;
     const uint64_t blocks = std::min<uint64_t>((uint64_t)s->sms * 2, (cnt_n + 2047) / 2048);
@@ -1400,7 +1403,8 @@ int ut_gather_host(const ut_table* ct, const int64_t* idx_host, uint64_t n, void
     if ((e = cudaMemcpyAsync(s->idx_buf[b], idx_host + off, cnt * sizeof(int64_t),
                              cudaMemcpyHostToDevice, st)) != cudaSuccess)
       return cuda_err(e, "cudaMemcpyAsync(idx H2D)");
-    if ((rc = gather_on(t, s, s->idx_buf[b], cnt, s->out_buf[b], st)) != UT_OK) return rc;
+    if ((rc = gather_on(t, s, s->idx_buf[b], cnt, s->out_buf[b], st, false, nullptr, off)) != UT_OK)
+      return rc;
     cudaEventRecord(s->gathered[b], st);
     cudaStreamWaitEvent(s->copy_stream, s->gathered[b], 0);
     if ((e = cudaMemcpyAsync((uint8_t*)out_host + off * t->rb, s->out_buf[b], cnt * t->rb,

@@ -165,6 +165,7 @@ struct GatherArgs {
   const uint32_t* perm;   // optional visiting order (work item j handles output row perm[j])
   const uint64_t* n_dev;  // optional: the row count lives in device memory (min(*n_dev, n))
   const CUtensorMap* tmap = nullptr;   // host copy of the table's tensor map ("tma4" plan only)
+  uint64_t pos0 = 0;      // position of idx[0] in the caller's list (chunked gathers' error record)
 };
 
 // The kernels' view of the arguments: n read from device memory when the launch is
@@ -186,8 +187,10 @@ __device__ __forceinline__ uint64_t row_of(const GatherArgs& a, uint64_t j, bool
   return inb ? (uint64_t)__ldg(a.perm + j) : 0ull;
 }
 
-__device__ __forceinline__ void record_bad(unsigned long long* err, uint64_t i) {
-  atomicMin(err, (unsigned long long)i);
+// Position i of this launch's list is out of range: keep the smallest position of the caller's
+// whole list (a.pos0 = where this launch's list starts in it, for chunked gathers).
+__device__ __forceinline__ void record_bad(const GatherArgs& a, uint64_t i) {
+  atomicMin(a.err, (unsigned long long)(a.pos0 + i));
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -215,7 +218,7 @@ __global__ void __launch_bounds__(256, UT_MINB) k_narrow(GatherArgs a_) {
       const uint64_t i = ii[u];
       if (inb[u]) {
         *reinterpret_cast<T*>(a.out + i * sizeof(T)) = v[u];
-        if (!ok[u]) record_bad(a.err, i);
+        if (!ok[u]) record_bad(a, i);
       }
     }
   }
@@ -280,7 +283,7 @@ __global__ void __launch_bounds__(256, UT_MINB) k_single(GatherArgs a_) {
           st_chunk_clip(D, funnel16(lo, hi, r), d, d + a.rb);
         }
       }
-      if (inb[u] && !ok[u] && q == 0) record_bad(a.err, i);
+      if (inb[u] && !ok[u] && q == 0) record_bad(a, i);
     }
   }
 }
@@ -345,7 +348,7 @@ __global__ void __launch_bounds__(256, UT_MINB) k_multi(GatherArgs a_) {
         }
       }
     }
-    if (!ok && lane == 0) record_bad(a.err, i);
+    if (!ok && lane == 0) record_bad(a, i);
   }
 }
 
@@ -402,7 +405,7 @@ __global__ void __launch_bounds__(256) k_staged(GatherArgs a_, uint32_t tile_row
       const int64_t r = __ldg(a.idx + r0 + k);
       const bool ok = (uint64_t)r < a.rows;
       src[k] = ok ? a.tbase + (uint64_t)r * a.rb : ~0ull;
-      if (!ok) record_bad(a.err, r0 + k);
+      if (!ok) record_bad(a, r0 + k);
     }
     __syncthreads();
     const uint32_t nch = nr * cpr;
@@ -506,7 +509,7 @@ __global__ void __launch_bounds__(256, 1) k_bulk(GatherArgs a_) {
             "l"(a.tbase + (uint64_t)r * a.rb), "r"((uint32_t)a.rb), "r"(bar)
             : "memory");
       }
-      if (lane == 0 && inb[u] && !ok) record_bad(a.err, i);
+      if (lane == 0 && inb[u] && !ok) record_bad(a, i);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -585,7 +588,7 @@ __global__ void __launch_bounds__(128, 1) k_tma4(const __grid_constant__ CUtenso
         if (i < a.n) {
           const int64_t r = __ldg(a.idx + i);
           if ((uint64_t)r < a.rows) crd = (int32_t)r;
-          else record_bad(a.err, i);
+          else record_bad(a, i);
         }
       }
       const int32_t c0 = __shfl_sync(0xffffffffu, crd, 0), c1 = __shfl_sync(0xffffffffu, crd, 1);
@@ -648,7 +651,7 @@ __global__ void __launch_bounds__(256) k_paper(GatherArgs a_) {
     uint32_t v = 0;
     if (ok) v = __ldg(reinterpret_cast<const uint32_t*>(a.tbase) + (uint64_t)g * W + e);
     reinterpret_cast<uint32_t*>(a.out)[r * W + e] = v;
-    if (!ok && j == 0) record_bad(a.err, r);
+    if (!ok && j == 0) record_bad(a, r);
   }
 }
 
@@ -810,7 +813,7 @@ __global__ void __launch_bounds__(256) k_runs(GatherArgs a_, const uint32_t* __r
     if (r0 >= a.rows) {        // an out-of-range index is a run of one: zero row + record
       const uint64_t d = a.out + i0 * a.rb;
       for (uint64_t c = (uint64_t)lane * 16; c < a.rb; c += 32 * 16) st16(d + c, v4_zero());
-      if (lane == 0) record_bad(a.err, i0);
+      if (lane == 0) record_bad(a, i0);
       continue;
     }
     const uint64_t s = a.tbase + r0 * a.rb;
@@ -937,7 +940,7 @@ __global__ void __launch_bounds__(256, UT_MINB) k_share(GatherArgs a_, ShareHash
         if (b < a.rb) st16(d + b, cur[u][c]);
         else st16(a.out + (nxt[u] - 1) * a.rb + (b - a.rb), cur[u][c]);
       }
-      if (!ok[u] && lane == 0) record_bad(a.err, ii[u]);
+      if (!ok[u] && lane == 0) record_bad(a, ii[u]);
     }
   }
 }

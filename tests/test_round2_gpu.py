@@ -567,22 +567,52 @@ def test_gather_beyond_2pow31_rows(rb, plan):
     workloads.fill_table(hb.addr, rows, rb, 601, threads=0)
     idx = workloads.uniform_idx(n, rows, 602)
     idx[-3:] = [rows - 1, 0, rows - 1]
+    # the only out-of-range ids lie past 2^31: the first one's WHOLE-LIST position must come back
+    # (the reorder's second 2^31-row chunk starts at 2^31)
+    first_bad = (1 << 31) + 7 + rb
+    idx[first_bad] = -1
+    idx[first_bad + 5] = rows
     with ut.Table(hb.addr, rows, rb) as t:
         t.set_plan(plan)
         idx_d = torch.from_numpy(idx).cuda()
         out = t.gather(idx_d)
-        assert t.error_pos() == -1
+        assert t.error_pos() == first_bad
         del idx_d
         got = out.cpu().numpy().reshape(n, rb)
         del out
     torch.cuda.empty_cache()
+    assert not got[[first_bad, first_bad + 5]].any()          # bad rows are zero-filled
+    idx[[first_bad, first_bad + 5]] = 0
+    got[[first_bad, first_bad + 5], :4] = 0
     ids = got[:, :4].copy().view(np.uint32).reshape(-1)
     assert np.array_equal(ids, idx.astype(np.uint32)), "a row id decodes wrong"
     del ids
     rng = np.random.default_rng(603)
     pos = np.concatenate([np.arange(1000), np.arange((1 << 31) - 1000, (1 << 31) + 1000),
                           np.arange(n - 1000, n), rng.integers(0, n, 1 << 20)])
+    pos = pos[(pos != first_bad) & (pos != first_bad + 5)]
     want, bad = oracle.gather(hb.addr, rows, rb, idx[pos])
     assert bad == -1
     assert got[pos].reshape(-1).tobytes() == want.tobytes()
+    hb.close()
+
+
+@pytest.mark.parametrize("pinned_out", [False, True])
+def test_gather_host_error_position_beyond_first_chunk(pinned_out):
+    """ut_gather_host reports the first out-of-range position of the WHOLE list, also when its
+    copy-engine path (pageable output) gathers in chunks of 8 MiB of rows: the bad ids sit in
+    later chunks; rows and the position match the oracle's."""
+    rows, rb, n = 10_000, 512, 100_000           # 16384 rows per chunk: 7 chunks
+    hb = workloads.HostBuffer(rows * rb)
+    workloads.fill_table(hb.addr, rows, rb, 701)
+    idx = workloads.uniform_idx(n, rows, 702)
+    idx[50_001] = rows
+    idx[70_000] = -1
+    want, bad = oracle.gather(hb.addr, rows, rb, idx)
+    assert bad == 50_001
+    out = torch.empty((n, rb), dtype=torch.uint8, pin_memory=pinned_out)
+    with ut.Table(hb.addr, rows, rb) as t:
+        t.gather_host(torch.from_numpy(idx), out_host=out)
+        assert out.numpy().reshape(-1).tobytes() == want.tobytes()
+        assert t.error_pos() == 50_001
     hb.close()
