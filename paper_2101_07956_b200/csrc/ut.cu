@@ -1287,6 +1287,14 @@ namespace {
 // address (UVA), and an unpinned stretch anywhere in the middle disqualifies the range — the
 // caller then refuses it instead of faulting. Where the driver reports no range extent, the first
 // and last bytes decide.
+// Error exit of ut_gather_host: wait for the copies already enqueued (they read the caller's idx
+// and write its output) without replacing the error message the caller is about to return.
+void drain_keep_error(cudaStream_t a, cudaStream_t b) {
+  cudaStreamSynchronize(a);
+  if (b) cudaStreamSynchronize(b);
+  cudaGetLastError();
+}
+
 bool host_range_mapped(uint64_t a, uint64_t bytes, const void* dev_ptr) {
   const uint64_t hi = a + bytes;
   const bool uva = (uint64_t)dev_ptr == a;
@@ -1357,7 +1365,10 @@ int ut_gather_host(const ut_table* ct, const int64_t* idx_host, uint64_t n, void
     if ((e = cudaMemcpyAsync(s->idx_all, idx_host, n * sizeof(int64_t), cudaMemcpyHostToDevice,
                              st)) != cudaSuccess)
       return cuda_err(e, "cudaMemcpyAsync(idx H2D)");
-    if ((rc = gather_on(t, s, s->idx_all, n, out_mapped, st, true)) != UT_OK) return rc;
+    if ((rc = gather_on(t, s, s->idx_all, n, out_mapped, st, true)) != UT_OK) {
+      drain_keep_error(st, nullptr);     // the idx copy may still read idx_host: finish it
+      return rc;
+    }
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_err(e, "sync stream");
     return UT_OK;
   }
@@ -1400,16 +1411,26 @@ int ut_gather_host(const ut_table* ct, const int64_t* idx_host, uint64_t n, void
     const int b = (int)(k % DevState::kBuf);
     const uint64_t cnt = std::min(per, n - off);
     if (k >= DevState::kBuf) cudaStreamWaitEvent(st, s->drained[b], 0);
+    // on an error after earlier chunks were enqueued, their copies still read idx_host and write
+    // out_host: finish them before returning, so the caller may free both
     if ((e = cudaMemcpyAsync(s->idx_buf[b], idx_host + off, cnt * sizeof(int64_t),
-                             cudaMemcpyHostToDevice, st)) != cudaSuccess)
-      return cuda_err(e, "cudaMemcpyAsync(idx H2D)");
-    if ((rc = gather_on(t, s, s->idx_buf[b], cnt, s->out_buf[b], st, false, nullptr, off)) != UT_OK)
+                             cudaMemcpyHostToDevice, st)) != cudaSuccess) {
+      rc = cuda_err(e, "cudaMemcpyAsync(idx H2D)");
+      drain_keep_error(st, s->copy_stream);
       return rc;
+    }
+    if ((rc = gather_on(t, s, s->idx_buf[b], cnt, s->out_buf[b], st, false, nullptr, off)) != UT_OK) {
+      drain_keep_error(st, s->copy_stream);
+      return rc;
+    }
     cudaEventRecord(s->gathered[b], st);
     cudaStreamWaitEvent(s->copy_stream, s->gathered[b], 0);
     if ((e = cudaMemcpyAsync((uint8_t*)out_host + off * t->rb, s->out_buf[b], cnt * t->rb,
-                             cudaMemcpyDeviceToHost, s->copy_stream)) != cudaSuccess)
-      return cuda_err(e, "cudaMemcpyAsync(rows D2H)");
+                             cudaMemcpyDeviceToHost, s->copy_stream)) != cudaSuccess) {
+      rc = cuda_err(e, "cudaMemcpyAsync(rows D2H)");
+      drain_keep_error(st, s->copy_stream);
+      return rc;
+    }
     cudaEventRecord(s->drained[b], s->copy_stream);
   }
   if ((e = cudaStreamSynchronize(s->copy_stream)) != cudaSuccess) return cuda_err(e, "sync copy stream");
