@@ -487,8 +487,13 @@ class Table:
         else:
             assert out.is_cuda and out.is_contiguous()
             assert out.numel() * out.element_size() >= n * self.row_bytes
+            assert out.device == idx.device
         go = ut_gather if idx.dtype == torch.int64 else ut_gather_i32
-        go(self.handle, idx.data_ptr(), n, out.data_ptr(), _stream_handle(stream))
+        # the C ABI gathers on the CURRENT device: make it the one idx and out live on, whatever
+        # the caller's current device is (and take that device's current stream by default)
+        with torch.cuda.device(idx.device):
+            go(self.handle, idx.data_ptr(), n, out.data_ptr(),
+               _stream_handle(stream if stream is not None else torch.cuda.current_stream(idx.device)))
         return out
 
     __getitem__ = gather
@@ -511,8 +516,11 @@ class Table:
 
     def gather_dn(self, idx, n_dev, out, stream=None):
         """Gather min(n_dev[0], idx.numel()) rows; the count is read on the device."""
-        ut_gather_dn(self.handle, idx.data_ptr(), n_dev.data_ptr(), idx.numel(), out.data_ptr(),
-                     _stream_handle(stream))
+        import torch
+        assert idx.device == n_dev.device == out.device
+        with torch.cuda.device(idx.device):
+            ut_gather_dn(self.handle, idx.data_ptr(), n_dev.data_ptr(), idx.numel(), out.data_ptr(),
+                         _stream_handle(stream if stream is not None else torch.cuda.current_stream(idx.device)))
         return out
 
     def gather_host(self, idx_host, out_host=None, stream=None):
