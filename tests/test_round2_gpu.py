@@ -553,7 +553,7 @@ def test_gather_int32_ids(rows, rb):
 
 
 @pytest.mark.timeout(900)
-@pytest.mark.parametrize("rb,plan", [(4, "auto"), (4, "reorder=off"), (16, "reorder=off")])
+@pytest.mark.parametrize("rb,plan", [(4, "auto"), (4, "reorder=off")])
 def test_gather_beyond_2pow31_rows(rb, plan):
     """Maximum sizes: one gather of n = 2^31 + 4099 rows (16 GiB of int64 ids in HBM) — past every
     32-bit row count. "auto" on this 256-MiB table of 4-B rows takes the reorder stage, which
