@@ -11,6 +11,8 @@ shares no code with it; both take their inputs from ``workloads`` only.
 * ``access_model`` is the paper's thread-per-element indexing kernel and its circular-shift
   variant written out as access traces, with the (warp, cacheline) request count the paper
   quotes (§4.5; Figs. 5/6). Pinned by the paper's 7 -> 5 example.
+* ``pool_model`` replays the unified allocator's block recycling (P:530-531 under SPEC's reading,
+  DESIGN.md R19). Pinned by tests/test_pool_model.py.
 """
 from __future__ import annotations
 
