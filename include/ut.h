@@ -108,11 +108,70 @@ UT_API ut_table* ut_register(const void* host_ptr, uint64_t rows, uint64_t row_b
 typedef enum ut_alloc_kind {
   UT_ALLOC_PINNED = 0,
   UT_ALLOC_MANAGED = 1,
-  UT_ALLOC_VMM_HOST = 2
+  UT_ALLOC_VMM_HOST = 2,
+  UT_ALLOC_SYSTEM = 3     /* ut_pool only: plain malloc, NOT GPU-mapped — exercises the pool's
+                             bookkeeping without a GPU; ut_create / ut_pool_table refuse it    */
 } ut_alloc_kind;
 
 UT_API ut_table* ut_create(const void* src, uint64_t rows, uint64_t row_bytes, int kind,
                            void** host_out);
+
+/*
+ * The unified allocator with block recycling (reading
+ * R19). PAPER.md §4.4: "A new memory allocator is implemented to govern the memory
+ * allocation for all unified tensors. It adapts the allocation recycling mechanism from the
+ * PyTorch CUDA allocator to reduce the number of CUDA API invocations."
+ *
+ * ut_pool_create — a pool of host blocks of one kind: UT_ALLOC_PINNED or UT_ALLOC_MANAGED (the
+ *   same backend calls and advice as ut_create, on the device current at this call), or
+ *   UT_ALLOC_SYSTEM (malloc; bookkeeping only, usable without a GPU). limit_bytes bounds the
+ *   bytes the pool holds from its backend, live + cached (0 = no limit). NULL on failure
+ *   (UT_EINVAL unknown kind / UT_ENOMEM / UT_ECUDA via ut_last_error).
+ * ut_pool_alloc — *host_out = a block of *capacity_out = bytes rounded up to a multiple of 512
+ *   (capacity_out may be NULL). The most recently freed cached block of exactly that capacity is
+ *   reused with no CUDA call; otherwise the backend allocates one. A backend allocation that would
+ *   pass limit_bytes (or that the backend refuses) first returns every cached block to the backend
+ *   and is retried once. bytes == 0 gives *host_out = NULL, capacity 0, no backend call. Blocks
+ *   are not zeroed. Returns UT_OK, UT_EINVAL (NULL pool / host_out), UT_ENOMEM or UT_ECUDA.
+ * ut_pool_free — cache a live block (never returned to the backend here); NULL is a no-op.
+ *   UT_EINVAL if host is not a live block of this pool (double free, foreign pointer). The caller
+ *   guarantees no GPU work still reads or writes the block (the pool does not synchronise).
+ * ut_pool_release_cached — return every cached block to the backend (cudaFreeHost / cudaFree).
+ * ut_pool_get_stats — counters, see ut_pool_stats.
+ * ut_pool_destroy — release the cached blocks and the pool. UT_EINVAL (pool unchanged) while
+ *   any block is live, including the blocks of live pool tables. NULL is a no-op.
+ * The pool is thread-safe (one mutex; backend calls happen under it).
+ */
+typedef struct ut_pool ut_pool;
+
+typedef struct ut_pool_stats {
+  uint64_t backend_calls;    /* fresh backend allocations (cudaHostAlloc / cudaMallocManaged)   */
+  uint64_t backend_frees;    /* blocks returned to the backend (release_cached, limit, destroy) */
+  uint64_t recycled_hits;    /* requests served from the cache                                 */
+  uint64_t bytes_live;       /* capacity of the blocks in use                                   */
+  uint64_t bytes_cached;     /* capacity of the cached blocks                                   */
+  uint64_t blocks_live;
+  uint64_t blocks_cached;
+  uint64_t limit_bytes;      /* as created; 0 = none                                            */
+} ut_pool_stats;
+
+UT_API ut_pool* ut_pool_create(int kind, uint64_t limit_bytes);
+UT_API int ut_pool_alloc(ut_pool* p, uint64_t bytes, void** host_out, uint64_t* capacity_out);
+UT_API int ut_pool_free(ut_pool* p, void* host);
+UT_API int ut_pool_release_cached(ut_pool* p);
+UT_API int ut_pool_get_stats(const ut_pool* p, ut_pool_stats* stats);
+UT_API int ut_pool_destroy(ut_pool* p);
+
+/*
+ * ut_pool_table — ut_create's table (`t.to("unified")`) over a block of pool p (kind PINNED or
+ * MANAGED): rows * row_bytes bytes taken with ut_pool_alloc, src copied in when not NULL,
+ * *host_out = the block. ut_release on the table hands the block back to p (cached, no CUDA free
+ * call); p must outlive the table. Mapping on other devices as for ut_create. Returns NULL on
+ * failure (UT_EINVAL: NULL p / host_out, zero rows or row_bytes, overflow, SYSTEM kind;
+ * UT_ENOMEM / UT_ECUDA / UT_ENOTSUP via ut_last_error).
+ */
+UT_API ut_table* ut_pool_table(ut_pool* p, const void* src, uint64_t rows, uint64_t row_bytes,
+                               void** host_out);
 
 /*
  * ut_gather — out_dev[i*rb .. (i+1)*rb) = row idx_dev[i] of the table, for i in [0, n).

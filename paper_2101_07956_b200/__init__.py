@@ -14,10 +14,13 @@ Low level (same names and arguments as the C ABI, raw addresses and ints):
     ut_table_get_info(handle) -> dict
     ut_coop_create / _export / _open / _dispatch / _fetch / _combine / _gather / _get_stats /
     _error_pos / _owner / _release (the cooperative multi-rank gather)
+    ut_pool_create / _alloc / _free / _release_cached / _get_stats / _destroy / _table (the
+    unified allocator with block recycling)
 
 High level: ``Table`` — the paper's unified tensor, ``Table(features)[gpu_idx]`` being
 ``unified_tensor[gpu_tensor]``; ``Coop`` — one rank's side of the cooperative
-gather (rows requested by several ranks cross the host link once); ``Graph`` — GPU sampling.
+gather (rows requested by several ranks cross the host link once); ``Graph`` — GPU sampling;
+``Pool`` — the recycling unified allocator (``Table.from_pool``).
 """
 from __future__ import annotations
 
@@ -37,11 +40,13 @@ ABI = ("ut_register", "ut_gather", "ut_gather_host", "ut_release", "ut_error_pos
        "ut_coop_open", "ut_coop_dispatch", "ut_coop_fetch", "ut_coop_combine", "ut_coop_gather",
        "ut_coop_get_stats", "ut_coop_error_pos", "ut_coop_owner", "ut_coop_release",
        "ut_coop_create_partitioned", "ut_coop_partition_ids", "ut_coop_open_local",
-       "ut_gather_multi", "ut_numa_interleave", "ut_gather_i32", "ut_numa_place")
+       "ut_gather_multi", "ut_numa_interleave", "ut_gather_i32", "ut_numa_place",
+       "ut_pool_create", "ut_pool_alloc", "ut_pool_free", "ut_pool_release_cached",
+       "ut_pool_get_stats", "ut_pool_destroy", "ut_pool_table")
 
 UT_COOP_HANDLE_BYTES = 64
 
-UT_ALLOC = {"pinned": 0, "managed": 1, "vmm": 2}
+UT_ALLOC = {"pinned": 0, "managed": 1, "vmm": 2, "system": 3}
 
 
 class UTError(RuntimeError):
@@ -63,6 +68,12 @@ class _Stats(ctypes.Structure):
                 ("rows", ctypes.c_uint64), ("bytes", ctypes.c_uint64),
                 ("timed_launches", ctypes.c_uint64), ("gather_kernel_ms", ctypes.c_double),
                 ("share_gathers", ctypes.c_uint64)]
+
+
+class _PoolStats(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint64) for k in ("backend_calls", "backend_frees", "recycled_hits",
+                                               "bytes_live", "bytes_cached", "blocks_live",
+                                               "blocks_cached", "limit_bytes")]
 
 
 class _CoopStats(ctypes.Structure):
@@ -99,6 +110,20 @@ def _load():
     L.ut_table_get_info.argtypes = [vp, ctypes.POINTER(_Info)]
     L.ut_create.restype = vp
     L.ut_create.argtypes = [vp, u64, u64, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]
+    L.ut_pool_create.restype = vp
+    L.ut_pool_create.argtypes = [ctypes.c_int, u64]
+    L.ut_pool_alloc.restype = ctypes.c_int
+    L.ut_pool_alloc.argtypes = [vp, u64, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(u64)]
+    L.ut_pool_free.restype = ctypes.c_int
+    L.ut_pool_free.argtypes = [vp, vp]
+    L.ut_pool_release_cached.restype = ctypes.c_int
+    L.ut_pool_release_cached.argtypes = [vp]
+    L.ut_pool_get_stats.restype = ctypes.c_int
+    L.ut_pool_get_stats.argtypes = [vp, ctypes.POINTER(_PoolStats)]
+    L.ut_pool_destroy.restype = ctypes.c_int
+    L.ut_pool_destroy.argtypes = [vp]
+    L.ut_pool_table.restype = vp
+    L.ut_pool_table.argtypes = [vp, vp, u64, u64, ctypes.POINTER(ctypes.c_void_p)]
     L.ut_graph_register.restype = vp
     L.ut_graph_register.argtypes = [vp, vp, u64, u64]
     L.ut_graph_set_option.restype = ctypes.c_int
@@ -190,6 +215,49 @@ def ut_create(src: int, rows: int, row_bytes: int, kind: int) -> tuple[int, int]
     """(handle, host address) of a new library-owned table (src 0/None: left for the caller)."""
     host = ctypes.c_void_p()
     h = _lib.ut_create(src or None, rows, row_bytes, kind, ctypes.byref(host))
+    if not h:
+        code, msg = last_error()
+        raise UTError(code, msg)
+    return h, int(host.value)
+
+
+def ut_pool_create(kind: int, limit_bytes: int = 0) -> int:
+    h = _lib.ut_pool_create(kind, limit_bytes)
+    if not h:
+        code, msg = last_error()
+        raise UTError(code, msg)
+    return h
+
+
+def ut_pool_alloc(p: int, nbytes: int) -> tuple[int, int]:
+    """(host address or 0, capacity) of a pool block."""
+    host, cap = ctypes.c_void_p(), ctypes.c_uint64()
+    _check(_lib.ut_pool_alloc(p, nbytes, ctypes.byref(host), ctypes.byref(cap)))
+    return int(host.value or 0), int(cap.value)
+
+
+def ut_pool_free(p: int, host: int) -> None:
+    _check(_lib.ut_pool_free(p, host or None))
+
+
+def ut_pool_release_cached(p: int) -> None:
+    _check(_lib.ut_pool_release_cached(p))
+
+
+def ut_pool_get_stats(p: int) -> dict:
+    st = _PoolStats()
+    _check(_lib.ut_pool_get_stats(p, ctypes.byref(st)))
+    return {k: getattr(st, k) for k, _ in st._fields_}
+
+
+def ut_pool_destroy(p: int) -> None:
+    _check(_lib.ut_pool_destroy(p))
+
+
+def ut_pool_table(p: int, src: int, rows: int, row_bytes: int) -> tuple[int, int]:
+    """(handle, host address) of a table over a pool block; ut_release gives the block back."""
+    host = ctypes.c_void_p()
+    h = _lib.ut_pool_table(p, src or None, rows, row_bytes, ctypes.byref(host))
     if not h:
         code, msg = last_error()
         raise UTError(code, msg)
@@ -449,6 +517,19 @@ class Table:
         self.rows, self.row_bytes = int(rows), int(row_bytes)
         return self
 
+    @classmethod
+    def from_pool(cls, pool: "Pool", rows: int, row_bytes: int, src=None) -> "Table":
+        """`Table.create` over a block of `pool` (the recycling unified allocator):
+        closing the table caches the block in the pool instead of freeing it."""
+        addr = None
+        if src is not None:
+            addr = src.ctypes.data if hasattr(src, "ctypes") else src.data_ptr()
+        self = cls.__new__(cls)
+        self._keep = (src, pool)                # the pool outlives its tables
+        self.handle, self.host_addr = ut_pool_table(pool.handle, addr, rows, row_bytes)
+        self.rows, self.row_bytes = int(rows), int(row_bytes)
+        return self
+
     def array(self):
         """uint8 numpy view of the table's host bytes (no copy)."""
         import numpy as np
@@ -550,6 +631,42 @@ class Table:
 
     def __exit__(self, *a):
         self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Pool:
+    """The unified allocator with block recycling (``ut_pool_*``): host
+    blocks of one kind ("pinned", "managed"; "system" = malloc, bookkeeping only) that are cached
+    on free and reused for the next request of the same 512-B-rounded size."""
+
+    def __init__(self, kind: str = "managed", limit_bytes: int = 0):
+        self.kind = kind
+        self.handle = ut_pool_create(UT_ALLOC[kind], limit_bytes)
+
+    def alloc(self, nbytes: int) -> tuple[int, int]:
+        return ut_pool_alloc(self.handle, nbytes)
+
+    def free(self, host: int) -> None:
+        ut_pool_free(self.handle, host)
+
+    def release_cached(self) -> None:
+        ut_pool_release_cached(self.handle)
+
+    def stats(self) -> dict:
+        return ut_pool_get_stats(self.handle)
+
+    def table(self, rows: int, row_bytes: int, src=None) -> Table:
+        return Table.from_pool(self, rows, row_bytes, src)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            ut_pool_destroy(self.handle)
+            self.handle = None
 
     def __del__(self):
         try:

@@ -10,7 +10,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libut.so")
-SOURCES = [os.path.join(CSRC, "ut.cu"), os.path.join(CSRC, "ut_sample.cu"), os.path.join(CSRC, "ut_coop.cu")]
+SOURCES = [os.path.join(CSRC, "ut.cu"), os.path.join(CSRC, "ut_sample.cu"), os.path.join(CSRC, "ut_coop.cu"),
+           os.path.join(CSRC, "ut_pool.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "ut_kernels.cuh"), os.path.join(CSRC, "ut_internal.h"),
                   os.path.join(CSRC, "ut_scan.cuh"),
                   os.path.join(INCLUDE, "ut.h")]

@@ -326,6 +326,7 @@ struct ut_table {
   int registered = 0, read_only = 0, device = 0;
   int alloc_kind = -1;                  // ut_create: ut_alloc_kind; -1 = caller memory
   bool direct_va = false;               // device address == host address (managed / VMM)
+  ut_pool* pool = nullptr;              // ut_pool_table: ut_release hands the block back
   unsigned long long vmm_handle = 0;    // CUmemGenericAllocationHandle
   uint64_t vmm_bytes = 0;
   PlanKind forced = P_AUTO;
@@ -1128,6 +1129,36 @@ void vmm_host_free(void* va, uint64_t size, unsigned long long handle) {
 
 }  // namespace
 
+namespace {
+
+// The table of a library-owned allocation p (ut_create, ut_pool_table): record it, set up the
+// creating device's state, hand out the host address. On failure the table and p are released.
+ut_table* finish_owned(ut_table* t, void* p, uint64_t rows, uint64_t row_bytes, int dev, int kind,
+                       ut_pool* pool, void** host_out) {
+  t->host = (const uint8_t*)p;
+  t->rows = rows;
+  t->rb = row_bytes;
+  t->bytes = rows * row_bytes;
+  t->device = dev;
+  t->alloc_kind = kind;
+  t->direct_va = kind != UT_ALLOC_PINNED;
+  t->pool = pool;
+  DevState* s;
+  if (dev_state(t, &s) != UT_OK) {
+    char msg[512];
+    int code = ut_last_error(msg, sizeof msg);
+    ut_release(t);
+    set_err(code, "%s", msg);
+    return nullptr;
+  }
+  *host_out = p;
+  g_err_code = UT_OK;
+  g_err_msg[0] = 0;
+  return t;
+}
+
+}  // namespace
+
 extern "C" {
 
 ut_table* ut_create(const void* src, uint64_t rows, uint64_t row_bytes, int kind, void** host_out) {
@@ -1143,34 +1174,9 @@ ut_table* ut_create(const void* src, uint64_t rows, uint64_t row_bytes, int kind
   unsigned long long vmm_h = 0;
   switch (kind) {
     case UT_ALLOC_PINNED:
-      if ((e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable | cudaHostAllocMapped)) != cudaSuccess) {
-        cudaGetLastError();
-        return set_err(UT_ENOMEM, "cudaHostAlloc(%llu): %s", (unsigned long long)bytes,
-                       cudaGetErrorString(e)), nullptr;
-      }
+    case UT_ALLOC_MANAGED:
+      if (utx::backend_alloc(kind, dev, bytes, &p) != UT_OK) return nullptr;
       break;
-    case UT_ALLOC_MANAGED: {
-      int managed = 0;
-      cudaDeviceGetAttribute(&managed, cudaDevAttrManagedMemory, dev);
-      if (!managed) return set_err(UT_ENOTSUP, "device %d has no managed memory", dev), nullptr;
-      if ((e = cudaMallocManaged(&p, bytes, cudaMemAttachGlobal)) != cudaSuccess) {
-        cudaGetLastError();
-        return set_err(UT_ENOMEM, "cudaMallocManaged(%llu): %s", (unsigned long long)bytes,
-                       cudaGetErrorString(e)), nullptr;
-      }
-      cudaMemLocation cpu{};
-      cpu.type = cudaMemLocationTypeHost;
-      cpu.id = 0;
-      cudaMemLocation gpu{};
-      gpu.type = cudaMemLocationTypeDevice;
-      gpu.id = dev;
-      if ((e = cudaMemAdvise(p, bytes, cudaMemAdviseSetPreferredLocation, cpu)) != cudaSuccess ||
-          (e = cudaMemAdvise(p, bytes, cudaMemAdviseSetAccessedBy, gpu)) != cudaSuccess) {
-        cudaFree(p);
-        return cuda_err(e, "cudaMemAdvise"), nullptr;
-      }
-      break;
-    }
     case UT_ALLOC_VMM_HOST:
       if (vmm_host_alloc(dev, bytes, &p, &vmm_size, &vmm_h) != UT_OK) return nullptr;
       break;
@@ -1180,32 +1186,33 @@ ut_table* ut_create(const void* src, uint64_t rows, uint64_t row_bytes, int kind
   if (src) memcpy(p, src, bytes);
   ut_table* t = new (std::nothrow) ut_table;
   if (!t) {
-    if (kind == UT_ALLOC_PINNED) cudaFreeHost(p);
-    else if (kind == UT_ALLOC_MANAGED) cudaFree(p);
-    else vmm_host_free(p, vmm_size, vmm_h);
+    if (kind == UT_ALLOC_VMM_HOST) vmm_host_free(p, vmm_size, vmm_h);
+    else utx::backend_free(kind, p);
     return set_err(UT_ENOMEM, "out of host memory"), nullptr;
   }
-  t->host = (const uint8_t*)p;
-  t->rows = rows;
-  t->rb = row_bytes;
-  t->bytes = bytes;
-  t->device = dev;
-  t->alloc_kind = kind;
-  t->direct_va = kind != UT_ALLOC_PINNED;
   t->vmm_handle = vmm_h;
   t->vmm_bytes = vmm_size;
-  DevState* s;
-  if (dev_state(t, &s) != UT_OK) {
-    char msg[512];
-    int code = ut_last_error(msg, sizeof msg);
-    ut_release(t);
-    set_err(code, "%s", msg);
-    return nullptr;
+  return finish_owned(t, p, rows, row_bytes, dev, kind, nullptr, host_out);
+}
+
+ut_table* ut_pool_table(ut_pool* pool, const void* src, uint64_t rows, uint64_t row_bytes,
+                        void** host_out) {
+  if (!pool || !host_out) return set_err(UT_EINVAL, "pool or host_out is NULL"), nullptr;
+  if (rows == 0 || row_bytes == 0) return set_err(UT_EINVAL, "rows and row_bytes must be >= 1"), nullptr;
+  if (rows > UINT64_MAX / row_bytes) return set_err(UT_EINVAL, "rows*row_bytes overflows"), nullptr;
+  const int kind = utx::pool_kind(pool);
+  if (kind != UT_ALLOC_PINNED && kind != UT_ALLOC_MANAGED)
+    return set_err(UT_EINVAL, "pool kind %d is not GPU-mapped", kind), nullptr;
+  void* p = nullptr;
+  if (utx::pool_take(pool, rows * row_bytes, &p, nullptr) != UT_OK) return nullptr;
+  if (src) memcpy(p, src, rows * row_bytes);
+  ut_table* t = new (std::nothrow) ut_table;
+  if (!t) {
+    utx::pool_give(pool, p);
+    return set_err(UT_ENOMEM, "out of host memory"), nullptr;
   }
-  *host_out = p;
-  g_err_code = UT_OK;
-  g_err_msg[0] = 0;
-  return t;
+  // the block's backend mapping was made on the pool's device; dev_state extends it to others
+  return finish_owned(t, p, rows, row_bytes, utx::pool_device(pool), kind, pool, host_out);
 }
 
 int ut_gather(const ut_table* t, const int64_t* idx_dev, uint64_t n, void* out_dev, ut_stream_t stream) {
@@ -1471,8 +1478,9 @@ int ut_release(ut_table* t) {
     cudaError_t e = cudaHostUnregister(const_cast<uint8_t*>(r.first));
     if (e != cudaSuccess) rc = cuda_err(e, "cudaHostUnregister");
   }
-  if (t->alloc_kind == UT_ALLOC_PINNED) cudaFreeHost(const_cast<uint8_t*>(t->host));
-  else if (t->alloc_kind == UT_ALLOC_MANAGED) cudaFree(const_cast<uint8_t*>(t->host));
+  if (t->pool) utx::pool_give(t->pool, const_cast<uint8_t*>(t->host));   // cached, not freed
+  else if (t->alloc_kind == UT_ALLOC_PINNED || t->alloc_kind == UT_ALLOC_MANAGED)
+    utx::backend_free(t->alloc_kind, const_cast<uint8_t*>(t->host));
   else if (t->alloc_kind == UT_ALLOC_VMM_HOST)
     vmm_host_free(const_cast<uint8_t*>(t->host), t->vmm_bytes, t->vmm_handle);
   delete t;

@@ -27,4 +27,22 @@ void unpin_host(Pin* pin);
 // Device address of host address `p` inside `pin` on the current device.
 int pin_device_ptr(const Pin& pin, const void* p, uint64_t* dev);
 
+// Host allocations of a ut_alloc_kind (PINNED, MANAGED with the paper's advice, SYSTEM) on
+// device `dev`: what ut_create and the recycling pool (ut_pool.cu) both call.
+int backend_alloc(int kind, int dev, uint64_t bytes, void** out);
+void backend_free(int kind, void* p);
+
+}  // namespace utx
+
+struct ut_pool;
+
+namespace utx {
+
+// The recycling pool's block interface (ut_pool.cu): take returns a block of >= bytes (capacity
+// in *cap), give caches it again; pool tables (ut_pool_table) hold one block each.
+int pool_take(ut_pool* p, uint64_t bytes, void** out, uint64_t* cap);
+int pool_give(ut_pool* p, void* block);
+int pool_kind(const ut_pool* p);
+int pool_device(const ut_pool* p);
+
 }  // namespace utx

@@ -14,6 +14,9 @@ top of the C ABI, without a PyTorch fork:
   ``is_unified`` / ``set_propagatedToCUDA`` / ``memAdvise`` accept any tensor and raise
   ``RuntimeError`` for non-unified ones.
 * ``resolve_placement(operands)`` — Table 3, the six cells.
+* Storage from the recycling unified allocator (§4.4; ``ut_pool_*``): a closed
+  tensor's block serves the next tensor of the same rounded size; ``allocator_stats()``,
+  ``empty_cache()``.
 * ``u[idx]`` — ``unified_tensor[gpu_tensor]``: the rows are gathered by ``ut_gather``
   (the hot path) straight out of host memory; output GPU or unified per Table 3.
 * Elementwise ``+ - * / < > <= >= ==`` with CPU tensors, GPU tensors, scalars and other unified
@@ -28,10 +31,36 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import Table, UTError, ut_mem_advise
+from . import Pool, Table, UTError, ut_mem_advise
 
 _ADVICE = {"SetPreferredLocation": 0, "UnsetPreferredLocation": 1, "SetAccessedBy": 2,
            "UnsetAccessedBy": 3, "SetReadMostly": 4, "UnsetReadMostly": 5}
+
+# ---- the unified allocator (§4.4) ---------------------------------------------
+# Every unified tensor's storage comes from one recycling pool per allocation kind: closing a
+# tensor caches its block, and the next tensor of the same 512-B-rounded size reuses it without a
+# cudaMallocManaged / cudaMemAdvise (or cudaHostAlloc) call — "adapts the allocation recycling
+# mechanism from the PyTorch CUDA allocator to reduce the number of CUDA API invocations".
+_POOLED = ("managed", "pinned")
+_pools: dict = {}
+
+
+def _pool(kind: str) -> Pool:
+    if kind not in _pools:
+        _pools[kind] = Pool(kind)
+    return _pools[kind]
+
+
+def allocator_stats(kind: str = "managed") -> dict:
+    """Counters of the unified allocator for ``kind`` (backend calls, recycled hits, bytes)."""
+    return _pool(kind).stats()
+
+
+def empty_cache() -> None:
+    """Return every cached unified block to CUDA (``torch.cuda.empty_cache`` for unified)."""
+    for p in _pools.values():
+        p.release_cached()
+
 
 # ---- Table 3 -------------------------------------------------------------------------------------
 GPU, CPU = "GPU", "CPU"
@@ -88,6 +117,8 @@ class UnifiedTensor:
         import torch
         self.shape = tuple(int(x) for x in shape)
         self.dtype = dtype
+        self.kind = kind
+        self.advise_record = None
         esize = torch.empty((), dtype=dtype).element_size()
         if len(self.shape) >= 2:      # rows = first dimension, as the paper's feature table
             rows, per_row = self.shape[0], int(np.prod(self.shape[1:]))
@@ -95,7 +126,10 @@ class UnifiedTensor:
             rows, per_row = int(np.prod(self.shape)), 1
         rows = max(1, rows)
         self.row_bytes = max(1, per_row * esize)
-        self.table = Table.create(rows, self.row_bytes, kind)
+        if kind in _POOLED:          # the recycling unified allocator (ut_pool_*)
+            self.table = Table.from_pool(_pool(kind), rows, self.row_bytes)
+        else:
+            self.table = Table.create(rows, self.row_bytes, kind)
         self.propagatedToCUDA = bool(propagatedToCUDA)
         self.advise_record = None
         if advise is not None:                      # right after allocation
@@ -205,7 +239,21 @@ class UnifiedTensor:
     __hash__ = object.__hash__
 
     def close(self) -> None:
+        if getattr(self, "table", None) is None or not self.table.handle:
+            return
+        if self.advise_record is not None and self.kind == "managed":
+            # the block goes back to the pool: restore the advice a fresh block has (Table 2)
+            dev = self.table.info()["device"]
+            for adv, where in (("UnsetReadMostly", "cpu"), ("SetPreferredLocation", "cpu"),
+                               ("SetAccessedBy", dev)):
+                ut_mem_advise(self.table.handle, _ADVICE[adv], _device_index(where))
         self.table.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def __repr__(self):
         return (f"UnifiedTensor(shape={self.shape}, dtype={self.dtype}, "
@@ -298,5 +346,6 @@ def memAdvise(t, advise: str, adviseDevice="cpu") -> int:
 
 
 __all__ = ["UnifiedTensor", "Operand", "resolve_placement", "to_unified", "unified", "is_unified",
+           "allocator_stats", "empty_cache",
            "set_propagatedToCUDA", "memAdvise", "GPU", "CPU", "OUT_GPU", "OUT_UNIFIED_PROP",
            "OUT_UNIFIED_NONPROP", "UTError"]

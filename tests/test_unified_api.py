@@ -127,3 +127,43 @@ def test_mem_advise_returns_cuda_error_codes():
     p = U.to_unified(x, kind="pinned")
     assert U.memAdvise(p, "SetReadMostly", "cpu") != 0   # not managed memory: the runtime's code
     assert p.cpu_view().equal(x)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["managed", "pinned"])
+def test_unified_tensors_recycle_their_blocks(kind):
+    """a closed unified tensor's block serves the next tensor of the same rounded size
+    with no new backend allocation; contents are the new tensor's, bit-exact."""
+    x = torch.randn(1000, 25)                            # 100 000 B -> 100 352-B block
+    u = U.to_unified(x, kind=kind)
+    addr = u.table.host_addr
+    before = U.allocator_stats(kind)
+    u.close()
+    y = torch.randn(1000, 25)
+    v = U.to_unified(y, kind=kind)
+    after = U.allocator_stats(kind)
+    assert v.table.host_addr == addr
+    assert after["backend_calls"] == before["backend_calls"]
+    assert after["recycled_hits"] == before["recycled_hits"] + 1
+    assert v.cpu_view().equal(y) and v.cuda_view().cpu().equal(y)
+    idx = torch.tensor([999, 0, 17, 17], device="cuda")
+    assert v[idx].cpu().equal(y[idx.cpu()])              # gathered from the recycled block
+    w = U.to_unified(torch.randn(10, 25), kind=kind)     # another size: a fresh block
+    assert U.allocator_stats(kind)["backend_calls"] == after["backend_calls"] + 1
+    v.close()
+    w.close()
+    U.empty_cache()
+    st = U.allocator_stats(kind)
+    assert st["blocks_cached"] == 0 and st["bytes_cached"] == 0
+
+
+@pytest.mark.gpu
+def test_advised_block_is_restored_before_reuse():
+    x = torch.randn(64, 64)
+    u = U.to_unified(x, advise="SetReadMostly", adviseDevice="cpu")
+    addr = u.table.host_addr
+    u.close()                                            # advice restored, block cached
+    v = U.to_unified(x)
+    assert v.table.host_addr == addr and v.cpu_view().equal(x)
+    assert v[torch.arange(64, device="cuda")].cpu().equal(x)
+    v.close()
