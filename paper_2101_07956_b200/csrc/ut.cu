@@ -357,6 +357,54 @@ int managed_accessed_by(const void* p, uint64_t bytes, int dev) {
   return UT_OK;
 }
 
+// Per-device resources every table of the process shares, so that a table costs no CUDA
+// allocation of its own (§6e: recycled unified tensors are tables too): one stream-ordered scratch
+// pool (reorder / share / int32 staging; trimmed when a table is released) and a slab of device
+// error words handed out and taken back by the tables.
+struct DevShared {
+  std::mutex mu;
+  cudaMemPool_t pool = nullptr;
+  std::vector<unsigned long long*> free_words;
+};
+DevShared g_shared[kMaxDev];
+constexpr int kWordsPerSlab = 4096;
+
+int shared_take(int dev, cudaMemPool_t* pool, unsigned long long** word) {
+  DevShared& d = g_shared[dev];
+  std::lock_guard<std::mutex> lk(d.mu);
+  cudaError_t e;
+  if (!d.pool) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    if ((e = cudaMemPoolCreate(&p, &props)) != cudaSuccess) return cuda_err(e, "cudaMemPoolCreate");
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+    d.pool = p;
+  }
+  if (d.free_words.empty()) {
+    unsigned long long* slab = nullptr;
+    if ((e = cudaMalloc(&slab, kWordsPerSlab * sizeof *slab)) != cudaSuccess)
+      return cuda_err(e, "cudaMalloc(error words)");
+    for (int i = kWordsPerSlab - 1; i >= 0; --i) d.free_words.push_back(slab + i);
+  }
+  unsigned long long* w = d.free_words.back();
+  if ((e = cudaMemset(w, 0xff, sizeof *w)) != cudaSuccess) return cuda_err(e, "cudaMemset(error word)");
+  d.free_words.pop_back();
+  *pool = d.pool;
+  *word = w;
+  return UT_OK;
+}
+
+void shared_give(int dev, unsigned long long* word) {
+  DevShared& d = g_shared[dev];
+  std::lock_guard<std::mutex> lk(d.mu);
+  d.free_words.push_back(word);
+  if (d.pool) cudaMemPoolTrimTo(d.pool, 0);   // the scratch a released table used goes back
+}
+
 // Map a VMM host allocation (cuMemCreate HOST_NUMA) for one more device.
 int vmm_grant(const void* va, uint64_t size, int dev) {
   using PAccess = CUresult (*)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
@@ -403,21 +451,10 @@ int dev_state(const ut_table* ct, DevState** out) {
       if (rc != UT_OK) return rc;
     }
     unsigned long long* err = nullptr;
-    e = cudaMalloc(&err, sizeof *err);
-    if (e != cudaSuccess) return cuda_err(e, "cudaMalloc(error word)");
-    e = cudaMemset(err, 0xff, sizeof *err);
-    if (e != cudaSuccess) return cuda_err(e, "cudaMemset(error word)");
+    cudaMemPool_t pool = nullptr;
+    if (int rc = shared_take(dev, &pool, &err)) return rc;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaMemPoolProps props{};
-    props.allocType = cudaMemAllocationTypePinned;
-    props.location.type = cudaMemLocationTypeDevice;
-    props.location.id = dev;
-    cudaMemPool_t pool = nullptr;
-    e = cudaMemPoolCreate(&pool, &props);
-    if (e != cudaSuccess) return cuda_err(e, "cudaMemPoolCreate");
-    uint64_t keep = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     s->pool = pool;
     s->dev_base = dev_base;
     s->err = err;
@@ -1454,7 +1491,6 @@ int ut_release(ut_table* t) {
     DevState& s = t->dev[d];
     if (!s.init && !s.copy_stream && !s.buf_rows) continue;
     cudaSetDevice(d);
-    if (s.err) cudaFree(s.err);
     for (int b = 0; b < DevState::kBuf; ++b) {
       if (s.idx_buf[b]) cudaFree(s.idx_buf[b]);
       if (s.out_buf[b]) cudaFree(s.out_buf[b]);
@@ -1468,10 +1504,7 @@ int ut_release(ut_table* t) {
         cudaEventDestroy(ev.first);
         cudaEventDestroy(ev.second);
       }
-    if (s.pool) {
-      cudaDeviceSynchronize();
-      cudaMemPoolDestroy(s.pool);
-    }
+    if (s.err) shared_give(d, s.err);   // no gather in flight (contract): the word is free
   }
   cudaSetDevice(cur);
   for (auto& r : t->pin.regs) {
