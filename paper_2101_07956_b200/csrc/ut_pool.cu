@@ -13,6 +13,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <mutex>
+#include <new>
 #include <unordered_map>
 #include <vector>
 
@@ -127,9 +128,9 @@ int pool_take(ut_pool* p, uint64_t bytes, void** out, uint64_t* cap_out) {
     *out = b;
     return UT_OK;
   }
-  if (p->limit && p->held + cap > p->limit) {       // R19: empty the cache, then retry once
+  if (p->limit && cap > p->limit - p->held) {       // R19: empty the cache, then retry once
     release_cached_locked(p);
-    if (p->held + cap > p->limit)
+    if (cap > p->limit - p->held)
       return set_err(UT_ENOMEM, "pool limit %llu B: %llu B held, %llu B requested",
                      (unsigned long long)p->limit, (unsigned long long)p->held,
                      (unsigned long long)cap);
