@@ -244,3 +244,50 @@ def test_gpu_pool_table_on_second_device_or_skip():
     assert np.array_equal(out.cpu().numpy().reshape(-1), exp)
     t.close()
     pool.close()
+
+
+@pytest.mark.gpu
+def test_gpu_pool_tables_from_threads_share_device_resources():
+    """Four host threads create, gather from and release pool tables at once on one device: the
+    tables' error words come from one shared slab and their scratch (line sharing, reorder) from
+    one shared stream-ordered pool that every release trims. Every gather == oracle, every
+    out-of-range id reported to its own table only."""
+    import threading
+
+    import torch
+    import oracle
+    import workloads
+    pool = ut.Pool("managed")
+    errors = []
+
+    def work(k):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            for it in range(6):
+                rows, rb = 20000 + 37 * k, (400, 512, 260)[(k + it) % 3]
+                with pool.table(rows, rb) as t:
+                    t.set_plan(("share=on", "reorder=on", "auto")[(k + it) % 3])
+                    workloads.fill_table(t.host_addr, rows, rb, seed=100 * k + it)
+                    idx = workloads.uniform_idx(30000, rows, seed=1000 * k + it)
+                    bad_at = 1234 + k if it % 2 else -1
+                    if bad_at >= 0:
+                        idx[bad_at] = rows + k          # this table's only out-of-range id
+                    want, want_bad = oracle.gather(t.host_addr, rows, rb, idx)
+                    with torch.cuda.stream(st):
+                        out = t.gather(torch.from_numpy(idx).cuda(), stream=st)
+                    st.synchronize()
+                    assert out.cpu().numpy().reshape(-1).tobytes() == want.tobytes()
+                    assert t.error_pos(stream=st) == want_bad == bad_at
+        except Exception as e:                           # noqa: BLE001 — reported below
+            errors.append(f"thread {k}: {e!r}")
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    st = pool.stats()
+    assert st["blocks_live"] == 0 and st["recycled_hits"] > 0
+    pool.close()
