@@ -291,3 +291,26 @@ def test_gpu_pool_tables_from_threads_share_device_resources():
     st = pool.stats()
     assert st["blocks_live"] == 0 and st["recycled_hits"] > 0
     pool.close()
+
+
+def test_ten_thousand_events_against_the_naive_allocator():
+    """SPEC acceptance criterion 6 (allocator recycling): 10,000 random alloc/free events on
+    the library's pool — capacities identical to the no-recycling allocator's, fewer or equal
+    backend calls, and the same decisions as the recycling model at every step."""
+    from oracle.pool_model import NaiveModel
+    ops = _ops(4242, n=10000)
+    pool, model, naive = ut.Pool("system"), PoolModel(), NaiveModel()
+    replay(pool, model, [o for o in ops if o[0] != "release"])
+    caps, ncaps, nid = {}, {}, {}
+    for o in ops:
+        if o[0] == "alloc":
+            nid[o[1]], ncaps[o[1]] = naive.allocate(o[2])
+            caps[o[1]] = pool.alloc(o[2])
+        elif o[0] == "free":
+            naive.free(nid[o[1]])
+            pool.free(caps[o[1]][0])
+    for tag in set(caps) - {o[1] for o in ops if o[0] == "free"}:
+        pool.free(caps[tag][0])
+    assert {t: c for t, (_, c) in caps.items()} == ncaps
+    assert pool.stats()["backend_calls"] <= naive.backend_calls
+    pool.close()
