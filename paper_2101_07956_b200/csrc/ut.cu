@@ -363,6 +363,7 @@ int managed_accessed_by(const void* p, uint64_t bytes, int dev) {
 // error words handed out and taken back by the tables.
 struct DevShared {
   std::mutex mu;
+  cudaStream_t stream = nullptr;        // private, non-blocking: clears a word and waits for it
   cudaMemPool_t pool = nullptr;
   std::vector<unsigned long long*> free_words;
 };
@@ -373,6 +374,8 @@ int shared_take(int dev, cudaMemPool_t* pool, unsigned long long** word) {
   DevShared& d = g_shared[dev];
   std::lock_guard<std::mutex> lk(d.mu);
   cudaError_t e;
+  if (!d.stream && (e = cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return cuda_err(e, "cudaStreamCreateWithFlags");
   if (!d.pool) {
     cudaMemPoolProps props{};
     props.allocType = cudaMemAllocationTypePinned;
@@ -391,7 +394,10 @@ int shared_take(int dev, cudaMemPool_t* pool, unsigned long long** word) {
     for (int i = kWordsPerSlab - 1; i >= 0; --i) d.free_words.push_back(slab + i);
   }
   unsigned long long* w = d.free_words.back();
-  if ((e = cudaMemset(w, 0xff, sizeof *w)) != cudaSuccess) return cuda_err(e, "cudaMemset(error word)");
+  // complete before the table is handed out: its first gather may run on any stream
+  if ((e = cudaMemsetAsync(w, 0xff, sizeof *w, d.stream)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(d.stream)) != cudaSuccess)
+    return cuda_err(e, "cudaMemsetAsync(error word)");
   d.free_words.pop_back();
   *pool = d.pool;
   *word = w;
@@ -1531,8 +1537,11 @@ int ut_error_pos(const ut_table* t, ut_stream_t stream, int64_t* first_bad) {
   if (e != cudaSuccess) return cuda_err(e, "cudaStreamSynchronize");
   e = cudaMemcpy(&v, s->err, sizeof v, cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_err(e, "cudaMemcpy(error word)");
-  e = cudaMemset(s->err, 0xff, sizeof v);
-  if (e != cudaSuccess) return cuda_err(e, "cudaMemset(error word)");
+  // cleared on `stream` and waited for: a gather enqueued after this call, on any stream, can
+  // not race the clear (cudaMemset on the legacy stream may still be pending at return)
+  e = cudaMemsetAsync(s->err, 0xff, sizeof v, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_err(e, "cudaMemsetAsync(error word)");
   if (v == ~0ull) {
     *first_bad = -1;
     return UT_OK;

@@ -637,7 +637,9 @@ int ut_coop_error_pos(const ut_coop* c, ut_stream_t stream, int64_t* first_bad) 
   if (e != cudaSuccess) return cuda_err(e, "cudaStreamSynchronize");
   unsigned long long v = 0;
   e = cudaMemcpy(&v, c->err, 8, cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess) e = cudaMemset(c->err, 0xff, 8);
+  // cleared on `stream` and waited for, so no later step races the clear
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->err, 0xff, 8, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_err(e, "error word");
   *first_bad = v == ~0ull ? -1 : (int64_t)v;
   return v == ~0ull ? UT_OK : UT_ERANGE;
