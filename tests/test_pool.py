@@ -314,3 +314,31 @@ def test_ten_thousand_events_against_the_naive_allocator():
     assert {t: c for t, (_, c) in caps.items()} == ncaps
     assert pool.stats()["backend_calls"] <= naive.backend_calls
     pool.close()
+
+
+@pytest.mark.gpu
+def test_recycled_error_word_starts_clear():
+    """A table released with an out-of-range id still recorded (never read by error_pos) hands
+    its error word back to the shared slab; the next table that takes the word — here the very
+    next one, on a non-blocking stream, gathering right away — reports no error of its own, and
+    then exactly its own."""
+    import torch
+    import oracle
+    import workloads
+    pool = ut.Pool("pinned")
+    rows, rb = 3000, 256
+    st = torch.cuda.Stream()                              # non-blocking
+    for it in range(50):
+        with pool.table(rows, rb) as t:
+            workloads.fill_table(t.host_addr, rows, rb, seed=it)
+            idx = workloads.uniform_idx(5000, rows, seed=it + 1)
+            if it % 2 == 0:
+                idx[17] = -5                              # left recorded at release
+            with torch.cuda.stream(st):
+                out = t.gather(torch.from_numpy(idx).cuda(), stream=st)
+            st.synchronize()
+            want, bad = oracle.gather(t.host_addr, rows, rb, idx)
+            assert out.cpu().numpy().reshape(-1).tobytes() == want.tobytes()
+            if it % 2:
+                assert t.error_pos(stream=st) == -1 == bad   # the previous table's error is gone
+    pool.close()
