@@ -1,5 +1,4 @@
 # round 2, last session: verification at HEAD after the stream-ordered error-word clears (driver order)
-# and the per-device shared table resources, plus the N>1 harness on this one GPU (oversubscribed)
 R=gpurun_out/r2fin7; mkdir -p $R
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $R/smoke.log 2>&1; echo "rc=$?" >> $R/smoke.log
 timeout 2400 python -m pytest tests -q -m gpu > $R/pytest_gpu.log 2>&1; echo "rc=$?" >> $R/pytest_gpu.log
