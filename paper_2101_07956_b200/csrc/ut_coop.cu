@@ -389,6 +389,7 @@ static ut_coop* coop_create(const ut_table* t, uint64_t full_rows, bool partitio
   if (e == cudaSuccess) e = cudaMalloc(&c->cnt, (uint64_t)world * 4);
   if (e == cudaSuccess) e = cudaMalloc(&c->err, 8);
   if (e == cudaSuccess) e = cudaMemset(c->err, 0xff, 8);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cudaStreamLegacy);   // memsets landed
   if (e != cudaSuccess) {
     cuda_err(e, "ut_coop_create allocation");
     ut_coop_release(c);
@@ -453,7 +454,10 @@ int ut_coop_open(ut_coop* c, const void* handles) {
     c->peer_host[q] = (uint8_t*)p;
     c->opened[q] = true;
   }
+  // from pageable memory cudaMemcpy may return before the DMA lands: wait for it, since the
+  // first step may run on a non-blocking stream
   cudaError_t e = cudaMemcpy(c->peers_dev, c->peer_host, sizeof(uint8_t*) * c->world, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cudaStreamLegacy);
   if (e != cudaSuccess) return cuda_err(e, "cudaMemcpy(peer table)");
   return UT_OK;
 }
@@ -486,7 +490,10 @@ int ut_coop_open_local(ut_coop* c, ut_coop* const* peers, int world) {
     c->peer_host[q] = p->region;    // not IPC-opened: ut_coop_release leaves it to its owner
     c->opened[q] = false;
   }
+  // from pageable memory cudaMemcpy may return before the DMA lands: wait for it, since the
+  // first step may run on a non-blocking stream
   cudaError_t e = cudaMemcpy(c->peers_dev, c->peer_host, sizeof(uint8_t*) * c->world, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cudaStreamLegacy);
   if (e != cudaSuccess) return cuda_err(e, "cudaMemcpy(peer table)");
   // In-process ranks wait for each other on the device (stream memory operations). Loading a
   // kernel lazily (CUDA_MODULE_LOADING=LAZY, the default) while another rank's stream of the

@@ -209,7 +209,8 @@ int graph_dev(ut_graph* g, ut_graph::Dev** out) {
       cudaGetLastError();
       return set_err(UT_ENOMEM, "HBM copy of indptr");
     }
-    if ((e = cudaMemcpy(s->indptr_copy, g->indptr, bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
+    if ((e = cudaMemcpy(s->indptr_copy, g->indptr, bytes, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(cudaStreamLegacy)) != cudaSuccess)   // landed before use
       return cuda_err(e, "indptr H2D");
   }
   if (g->indices_hbm && !s->indices_copy) {
@@ -218,7 +219,8 @@ int graph_dev(ut_graph* g, ut_graph::Dev** out) {
       cudaGetLastError();
       return set_err(UT_ENOMEM, "HBM copy of indices (%llu bytes)", (unsigned long long)bytes);
     }
-    if ((e = cudaMemcpy(s->indices_copy, g->indices, bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
+    if ((e = cudaMemcpy(s->indices_copy, g->indices, bytes, cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(cudaStreamLegacy)) != cudaSuccess)   // landed before use
       return cuda_err(e, "indices H2D");
   }
   *out = s;
