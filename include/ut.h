@@ -254,7 +254,8 @@ UT_API int ut_gather_host(const ut_table* t, const int64_t* idx_host, uint64_t n
  * ut_release — free the handle; unregister the memory iff ut_register registered it; free a
  * ut_create table's memory, or hand a ut_pool_table's block back to its pool (cached).
  * The table's device error words return to the per-device slab every table of the process
- * shares, and the shared stream-ordered scratch pool is trimmed. NULL is a no-op returning UT_OK.
+ * shares; the shared stream-ordered scratch pool is trimmed when the device's last table goes.
+ * NULL is a no-op returning UT_OK.
  * Must not be called while a gather on the table is in flight.
  */
 UT_API int ut_release(ut_table* t);

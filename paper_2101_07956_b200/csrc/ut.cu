@@ -359,13 +359,14 @@ int managed_accessed_by(const void* p, uint64_t bytes, int dev) {
 
 // Per-device resources every table of the process shares, so that a table costs no CUDA
 // allocation of its own (§6e: recycled unified tensors are tables too): one stream-ordered scratch
-// pool (reorder / share / int32 staging; trimmed when a table is released) and a slab of device
-// error words handed out and taken back by the tables.
+// pool (reorder / share / int32 staging; trimmed when the device's last table is released) and a
+// slab of device error words handed out and taken back by the tables.
 struct DevShared {
   std::mutex mu;
   cudaStream_t stream = nullptr;        // private, non-blocking: clears a word and waits for it
   cudaMemPool_t pool = nullptr;
   std::vector<unsigned long long*> free_words;
+  uint64_t tables = 0;                  // tables holding a word on this device
 };
 DevShared g_shared[kMaxDev];
 constexpr int kWordsPerSlab = 4096;
@@ -399,6 +400,7 @@ int shared_take(int dev, cudaMemPool_t* pool, unsigned long long** word) {
       (e = cudaStreamSynchronize(d.stream)) != cudaSuccess)
     return cuda_err(e, "cudaMemsetAsync(error word)");
   d.free_words.pop_back();
+  d.tables += 1;
   *pool = d.pool;
   *word = w;
   return UT_OK;
@@ -408,7 +410,9 @@ void shared_give(int dev, unsigned long long* word) {
   DevShared& d = g_shared[dev];
   std::lock_guard<std::mutex> lk(d.mu);
   d.free_words.push_back(word);
-  if (d.pool) cudaMemPoolTrimTo(d.pool, 0);   // the scratch a released table used goes back
+  d.tables -= 1;
+  // the last table of the device gone: its scratch goes back (live tables keep theirs warm)
+  if (d.pool && d.tables == 0) cudaMemPoolTrimTo(d.pool, 0);
 }
 
 // Map a VMM host allocation (cuMemCreate HOST_NUMA) for one more device.
