@@ -342,3 +342,32 @@ def test_recycled_error_word_starts_clear():
             if it % 2:
                 assert t.error_pos(stream=st) == -1 == bad   # the previous table's error is gone
     pool.close()
+
+
+try:
+    from hypothesis import given, settings, strategies as hs
+except ImportError:                                      # pragma: no cover
+    given = None
+
+if given is not None:
+    _op = hs.one_of(hs.tuples(hs.just("alloc"), hs.integers(0, 6000)),
+                    hs.tuples(hs.just("free"), hs.integers(0, 50)),
+                    hs.tuples(hs.just("release"), hs.just(0)))
+
+    @settings(max_examples=150, deadline=None)
+    @given(ops=hs.lists(_op, max_size=60), limit=hs.sampled_from([0, 4096, 10240]))
+    def test_system_pool_property(ops, limit):
+        """Any alloc / free / release sequence, with or without a byte limit: the library's pool
+        takes the model's decisions (same capacities, same reuse, same errors, same counters)."""
+        seq, live = [], []
+        for kind, v in ops:
+            if kind == "alloc":
+                seq.append(("alloc", len(seq), v))
+                live.append(len(seq) - 1)
+            elif kind == "free" and live:
+                seq.append(("free", live.pop(v % len(live))))
+            elif kind == "release":
+                seq.append(("release",))
+        pool = ut.Pool("system", limit_bytes=limit)
+        replay(pool, PoolModel(limit=limit), seq)
+        pool.close()
